@@ -1,0 +1,175 @@
+/*
+ * tframe_fse.h — C-ABI of the B200-native FSE-lite hot path (libtframe_b200.so).
+ *
+ * Drop-in boundary for the reference's per-tile extrapolator and tiling
+ * interface (tframe, arXiv 2207.00238 reference at /root/reference/proj):
+ *
+ *   reference interface (file:line)                       replaced by
+ *   ----------------------------------------------------  ------------------------------
+ *   tframe::plan_proposed(W,H,N)       tiling.hpp:99-111  tf_plan_proposed
+ *   tframe::plan(Strategy::proposed..) tiling.hpp:301     tf_plan_proposed
+ *   tframe::interior_boundary          tiling.hpp:231     tf_interior_boundary
+ *   tframe::expand(tile,d,W,H)         overlap.hpp:25-34  tf_expand
+ *   detail::check_fse_params           extrapolate.hpp:102 tf_check_fse_params
+ *   registry_lookup("fse-lite",params) extrapolate.hpp:418 tf_fse_params_from_string
+ *   FseLiteExtrapolator::params_string extrapolate.hpp:403 tf_fse_params_to_string
+ *   FseLiteExtrapolator::influence_radius extrapolate.hpp:397 tf_influence_radius
+ *   Extrapolator::extrapolate(img,mask) extrapolate.hpp:32 /
+ *     fse_lite_extrapolate             extrapolate.hpp:263 tf_fse_extrapolate
+ *   run_master / run_local             runtime.hpp:75,142 tf_tiled_extrapolate
+ *   (blocks processed, FseLiteTrace::residual_energy.size()) tf_count_blocks
+ *
+ * Conventions: plain C, caller-owned buffers, no exceptions cross the
+ * boundary.  Images are 8-bit row-major (stride = width, frames stacked);
+ * masks are 8-bit, nonzero = known (image.hpp:53, PixelMask).  Every entry
+ * point returns a tf_status; tf_last_error() gives the message of the last
+ * failure on the calling thread.  Status codes mirror the reference's error
+ * taxonomy / CLI exit codes (error.hpp:9-36, tools/main.cpp:18-22):
+ * std::invalid_argument -> TF_EINVAL, TilingError -> TF_ETILING (exit code 4).
+ *
+ * There is no CPU fallback: compute entry points fail with TF_ECUDA when no
+ * usable sm_100 device is present.
+ */
+#ifndef TFRAME_FSE_H
+#define TFRAME_FSE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_ABI_VERSION 1
+
+typedef enum tf_status {
+  TF_OK = 0,
+  TF_EINVAL = 1,       /* std::invalid_argument (params, dims)            */
+  TF_EIO = 2,          /* reserved (IoError)                              */
+  TF_EPROTO = 3,       /* reserved (ProtocolError / TransportError)       */
+  TF_ETILING = 4,      /* TilingError: degenerate tiling                  */
+  TF_ECUDA = 5,        /* CUDA runtime failure / no sm_100 device         */
+  TF_ENCCL = 6,        /* NCCL failure                                    */
+  TF_ENOMEM = 7,       /* host or device allocation failure               */
+  TF_EUNSUPPORTED = 8  /* support window larger than the kernel handles   */
+} tf_status;
+
+/* Arithmetic mode of the FSE kernel. */
+typedef enum tf_mode {
+  TF_MODE_EXACT = 0, /* IEEE binary64, reference operation order, no FMA:
+                        output byte-identical to the reference CPU FSE   */
+  TF_MODE_FAST = 1   /* binary64 with FMA contraction in the spectral
+                        update: within the stated tolerance             */
+} tf_mode;
+
+/* tiling.hpp:16-27 (Rect) */
+typedef struct tf_rect {
+  int32_t x, y, w, h;
+} tf_rect;
+
+/* extrapolate.hpp:86-92 (FseLiteParams): block_size, support_margin,
+ * model_iterations, compensation (gamma), weight_decay (rho). */
+typedef struct tf_fse_params {
+  int32_t block;
+  int32_t margin;
+  int32_t iters;
+  double gamma;
+  double rho;
+} tf_fse_params;
+
+/* runtime.hpp:25-33 (RunStats) plus device-side counters. */
+typedef struct tf_run_stats {
+  int64_t plan_us;
+  int64_t distribute_us;   /* H2D + launch issue                              */
+  int64_t compute_span_us; /* dispatch end -> last GPU done                   */
+  int64_t merge_us;        /* gather + D2H                                    */
+  int64_t total_us;
+  int64_t overhead_pixels; /* sum of halo minus core areas (overlap.hpp:21)  */
+  int64_t blocks_reference;/* blocks the reference processes (all halo blocks
+                              holding an unknown pixel, extrapolate.hpp:282) */
+  int64_t blocks_processed;/* blocks the GPU ran: unknown pixel inside a core */
+  double kernel_ms;        /* FSE kernel device time, max over GPUs           */
+  double flops;            /* sum of F_b over processed blocks  */
+  int64_t iterations;      /* sum of executed iterations I_b                  */
+  int64_t pixels_evaluated;/* unknown core pixels written by the model        */
+} tf_run_stats;
+
+typedef struct tf_ctx tf_ctx;
+
+/* ---- library / context ------------------------------------------------ */
+int tf_abi_version(void);
+/* n_gpus >= 1; device_ids may be NULL (devices 0..n_gpus-1).  Returns NULL on
+ * failure (see tf_last_error(NULL)). */
+tf_ctx* tf_create(int n_gpus, const int* device_ids);
+void tf_destroy(tf_ctx* ctx);
+const char* tf_last_error(const tf_ctx* ctx);
+int tf_set_mode(tf_ctx* ctx, int mode);
+int tf_get_mode(const tf_ctx* ctx);
+int tf_device_count(int* out);
+
+/* ---- parameters (registry semantics, extrapolate.hpp:342-437) ----------- */
+int tf_check_fse_params(const tf_fse_params* p);
+/* "block=..,margin=..,iters=..,gamma=..,rho=.." ; margin defaults to 2*block */
+int tf_fse_params_from_string(const char* s, tf_fse_params* out);
+int tf_fse_params_to_string(const tf_fse_params* p, char* buf, int buf_len);
+int tf_influence_radius(const tf_fse_params* p);
+
+/* ---- tiling (bit-exact with the reference) ------------------------------ */
+int tf_plan_proposed(int W, int H, int N, tf_rect* out_tiles /* N */);
+int tf_expand(const tf_rect* core, int d, int W, int H, tf_rect* out_halo);
+long long tf_interior_boundary(const tf_rect* tiles, int n);
+/* Blocks fse_lite_extrapolate processes on a w x h image (raster B-grid from
+ * (0,0), blocks holding an unknown pixel); host-side, no GPU needed. */
+int64_t tf_count_blocks(const uint8_t* known, int w, int h, int block);
+
+/* ---- extrapolation ------------------------------------------------------- */
+/* Extrapolator::extrapolate on one image: host buffers, synchronous. */
+int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int w, int h,
+                       const tf_fse_params* p, uint8_t* out);
+
+/* run_master equivalent: plan -> expand -> FSE per halo -> crop -> merge, for
+ * `frames` stacked W x H frames.  Tiles (frame-major) are spread over the
+ * context's GPUs round-robin (runtime.hpp:102); cores are gathered to the
+ * first GPU over NCCL, then copied to `out`.  Output is independent of the
+ * GPU count.  stats may be NULL. */
+int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                         int frames, int tiles, int overlap, const tf_fse_params* p,
+                         uint8_t* out, tf_run_stats* stats);
+
+/* Device-resident variant on GPU `gpu` of the context: d_img/d_known/d_out
+ * are device pointers on that GPU (d_out may alias nothing else); work is
+ * enqueued on `stream` (a cudaStream_t, NULL = the context's stream) and NOT
+ * synchronised (graph-capturable).  Only tiles t with t % n_parts == part
+ * are computed (part/n_parts implement a multi-rank split; 0/1 = all);
+ * known pixels of the whole image are copied to d_out.  stats may be NULL
+ * (filling it synchronises the stream). */
+int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img,
+                                const uint8_t* d_known, int W, int H, int frames, int tiles,
+                                int overlap, const tf_fse_params* p, int part, int n_parts,
+                                uint8_t* d_out, void* stream, tf_run_stats* stats);
+
+/* ---- multi-rank (one process per GPU, NCCL over NVLink) ------------------ */
+/* 128-byte NCCL unique id, to be broadcast by the caller's bootstrap. */
+int tf_comm_unique_id(uint8_t id[128]);
+/* Attach an NCCL communicator to a single-GPU context. */
+int tf_comm_init(tf_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
+/* Gather each rank's `bytes` at d_send into d_recv on `root` (rank-major,
+ * nranks*bytes); non-root ranks may pass d_recv = NULL. */
+int tf_comm_gather(tf_ctx* ctx, const void* d_send, void* d_recv, int64_t bytes, int root,
+                   void* stream);
+/* Gather the cores of tiles owned by each rank (t % nranks == rank) from every
+ * rank's d_img-sized buffer into root's d_out (same layout).  Packs, gathers
+ * and unpacks on device. */
+int tf_comm_gather_cores(tf_ctx* ctx, uint8_t* d_out, int W, int H, int frames, int tiles,
+                         int root, void* stream);
+
+/* ---- synthetic inputs (versioned generator) ---------------- */
+#define TF_SYNTH_VERSION 1
+/* config in 1..5 (BASELINE configs); fills one W x H frame of image + mask
+ * (mask 1 = known).  Seeds: image 1000*config + frame, mask that + 500. */
+int tf_synth_frame(int config, int frame, int W, int H, uint8_t* img, uint8_t* known);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TFRAME_FSE_H */

@@ -1,0 +1,272 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle bindings.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+leg may import this package, and only as the CHECKER (or the timed CPU
+reference arm).  The product (paper_2207_00238_b200) never imports it.
+
+Two oracles:
+  * Restatement (liboracle.so, fse_oracle.c): plain-C FSE-lite + tiling with
+    per-block instrumentation; always buildable (gcc), travels to the GPU box.
+  * Reference (_ref/libtframe_ref.so, ref_shim.cpp): the UNMODIFIED reference
+    headers compiled from /root/reference by oracle/Makefile; built here and
+    shipped prebuilt to the GPU box (git-ignored, not gpurun-ignored).
+Parity pin: tests/test_oracle.py checks the restatement byte-for-byte against
+the reference library and against tests/golden/ fixtures the reference made.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libtframe_ref.so"
+
+
+class orc_params(C.Structure):
+    _fields_ = [("block", C.c_int32), ("margin", C.c_int32), ("iters", C.c_int32),
+                ("gamma", C.c_double), ("rho", C.c_double)]
+
+
+class orc_block_stats(C.Structure):
+    _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("M", C.c_int32), ("L", C.c_int32),
+                ("iters", C.c_int32), ("pairs", C.c_int32), ("touched", C.c_int32),
+                ("unknown", C.c_int32), ("min_gap", C.c_double)]
+
+
+_orc = None
+_ref = None
+
+
+def _u8(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a)
+    if a.dtype != np.uint8:
+        a = (a != 0).astype(np.uint8) if a.dtype == bool else a.astype(np.uint8)
+    return a
+
+
+def orc() -> C.CDLL:
+    global _orc
+    if _orc is None:
+        if not ORACLE_LIB.exists():
+            raise RuntimeError(f"{ORACLE_LIB} missing: run `make -C oracle`")
+        L = C.CDLL(str(ORACLE_LIB))
+        L.orc_plan_proposed.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.orc_expand.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.orc_fse_lite.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(orc_params),
+                                   C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.orc_tiled.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.POINTER(orc_params), C.c_void_p, C.c_void_p]
+        L.orc_check_params.argtypes = [C.POINTER(orc_params)]
+        _orc = L
+    return _orc
+
+
+def have_ref() -> bool:
+    return REF_LIB.exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            raise RuntimeError(f"{REF_LIB} missing: run `make -C oracle ref` where /root/reference exists")
+        L = C.CDLL(str(REF_LIB))
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_plan_proposed.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.ref_interior_boundary.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.ref_interior_boundary.restype = C.c_longlong
+        L.ref_expand.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.ref_fse_lite.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_double, C.c_double, C.c_void_p, C.POINTER(C.c_int64)]
+        L.ref_fse_lite_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int64,
+                                         C.POINTER(C.c_int64)]
+        L.ref_registry.argtypes = [C.c_char_p, C.c_char_p] + [C.POINTER(C.c_int)] * 3 + \
+            [C.POINTER(C.c_double)] * 2 + [C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ref_run_local.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_void_p,
+                                    C.POINTER(C.c_int64)]
+        L.ref_tiled_allcores.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_void_p]
+        L.ref_gen_scatter_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_void_p]
+        L.ref_make_scene.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_void_p]
+        L.ref_psnr.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.ref_psnr.restype = C.c_double
+        L.ref_ssim.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.ref_ssim.restype = C.c_double
+        _ref = L
+    return _ref
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"oracle status {code} {msg}")
+        self.code = code
+
+
+# ------------------------------------------------------------------ restatement
+def plan_proposed(W, H, N):
+    out = np.zeros((max(N, 1), 4), np.int32)
+    rc = orc().orc_plan_proposed(W, H, N, out.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return out[:N]
+
+
+def expand(core, d, W, H):
+    c = np.asarray(core, np.int32)
+    h = np.zeros(4, np.int32)
+    rc = orc().orc_expand(c.ctypes.data, d, W, H, h.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return h
+
+
+def fse_lite(img, known, block, margin, iters, gamma, rho, with_stats=False):
+    """Restated fse_lite_extrapolate (extrapolate.hpp:263).  Returns out, or
+    (out, stats structured array) with per-block I_b, P_b, T_b, U_b, min gap."""
+    img = _u8(img)
+    kn = _u8(known)
+    h, w = img.shape
+    out = np.empty_like(img)
+    p = orc_params(block, margin, iters, gamma, rho)
+    nb = C.c_int64(0)
+    cap = ((w + block - 1) // block) * ((h + block - 1) // block) if with_stats else 0
+    st = (orc_block_stats * max(cap, 1))()
+    rc = orc().orc_fse_lite(img.ctypes.data, kn.ctypes.data, w, h, C.byref(p), out.ctypes.data,
+                            C.cast(st, C.c_void_p) if with_stats else None, cap, C.byref(nb))
+    if rc:
+        raise OracleError(rc)
+    if not with_stats:
+        return out
+    arr = np.ctypeslib.as_array(st)[: nb.value].copy()
+    return out, arr
+
+
+def tiled(img, known, tiles, overlap, block, margin, iters, gamma, rho):
+    """Restated run_master: returns (out, processed blocks per (frame, tile))."""
+    img = _u8(img)
+    kn = _u8(known)
+    if img.ndim == 2:
+        frames, (H, W) = 1, img.shape
+    else:
+        frames, H, W = img.shape
+    out = np.empty_like(img)
+    bpt = np.zeros(frames * tiles, np.int64)
+    p = orc_params(block, margin, iters, gamma, rho)
+    rc = orc().orc_tiled(img.ctypes.data, kn.ctypes.data, W, H, frames, tiles, overlap, C.byref(p),
+                         out.ctypes.data, bpt.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return out, bpt
+
+
+# ------------------------------------------------------------------ reference
+def ref_error() -> str:
+    return ref().ref_last_error().decode()
+
+
+def ref_plan_proposed(W, H, N):
+    out = np.zeros((max(N, 1), 4), np.int32)
+    rc = ref().ref_plan_proposed(W, H, N, out.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out[:N]
+
+
+def ref_expand(core, d, W, H):
+    c = np.asarray(core, np.int32)
+    h = np.zeros(4, np.int32)
+    rc = ref().ref_expand(c.ctypes.data, d, W, H, h.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return h
+
+
+def ref_fse_lite(img, known, block, margin, iters, gamma, rho, count_blocks=False):
+    img = _u8(img)
+    kn = _u8(known)
+    h, w = img.shape
+    out = np.empty_like(img)
+    nb = C.c_int64(0)
+    rc = ref().ref_fse_lite(img.ctypes.data, kn.ctypes.data, w, h, block, margin, iters, gamma, rho,
+                            out.ctypes.data, C.byref(nb) if count_blocks else None)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return (out, nb.value) if count_blocks else out
+
+
+def ref_run_local(img, known, tiles, overlap, block, margin, iters, gamma, rho, workers):
+    img = _u8(img)
+    kn = _u8(known)
+    H, W = img.shape
+    out = np.empty_like(img)
+    us = C.c_int64(0)
+    rc = ref().ref_run_local(img.ctypes.data, kn.ctypes.data, W, H, tiles, overlap, block, margin,
+                             iters, gamma, rho, workers, out.ctypes.data, C.byref(us))
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out, us.value
+
+
+def ref_tiled_allcores(img, known, tiles, overlap, block, margin, iters, gamma, rho,
+                       threads=None, band_blocks=1, out=None):
+    img = _u8(img)
+    kn = _u8(known)
+    if img.ndim == 2:
+        frames, (H, W) = 1, img.shape
+    else:
+        frames, H, W = img.shape
+    if out is None:
+        out = img.copy()
+    threads = threads or os.cpu_count() or 1
+    rc = ref().ref_tiled_allcores(img.ctypes.data, kn.ctypes.data, W, H, frames, tiles, overlap,
+                                  block, margin, iters, gamma, rho, threads, band_blocks,
+                                  out.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out
+
+
+def ref_registry(name, params=""):
+    b, m, i = C.c_int(0), C.c_int(0), C.c_int(0)
+    g, r = C.c_double(0), C.c_double(0)
+    infl = C.c_int(0)
+    buf = C.create_string_buffer(256)
+    rc = ref().ref_registry(name.encode(), params.encode(), C.byref(b), C.byref(m), C.byref(i),
+                            C.byref(g), C.byref(r), C.byref(infl), buf, 256)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return dict(block=b.value, margin=m.value, iters=i.value, gamma=g.value, rho=r.value,
+                influence=infl.value, params_string=buf.value.decode())
+
+
+def ref_gen_scatter_mask(w, h, fraction, block, seed):
+    out = np.empty((h, w), np.uint8)
+    rc = ref().ref_gen_scatter_mask(w, h, fraction, block, seed, out.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out
+
+
+def ref_make_scene(w, h, seed):
+    out = np.empty((h, w), np.uint8)
+    ref().ref_make_scene(w, h, seed, out.ctypes.data)
+    return out
+
+
+def ref_psnr(a, b):
+    a, b = _u8(a), _u8(b)
+    return ref().ref_psnr(a.ctypes.data, b.ctypes.data, a.shape[1], a.shape[0])
+
+
+def psnr(a, b) -> float:
+    """metrics.hpp:327-335 (restated; used where the reference lib is absent)."""
+    d = a.astype(np.float64) - b.astype(np.float64)
+    mse = float(np.mean(d * d))
+    return float("inf") if mse == 0.0 else 10.0 * np.log10(255.0 * 255.0 / mse)

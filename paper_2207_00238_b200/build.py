@@ -1,0 +1,72 @@
+"""Build the sm_100a C-ABI library (and, for tests, the CPU oracle).
+
+    python -m paper_2207_00238_b200.build          # libtframe_b200.so
+    python -m paper_2207_00238_b200.build --oracle # + oracle/liboracle.so (+ oracle/_ref if /root/reference exists)
+
+The library is built IN-TREE (paper_2207_00238_b200/_lib/) so that it travels
+with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIBDIR = PKG / "_lib"
+LIB = LIBDIR / "libtframe_b200.so"
+SOURCES = ["fse_kernels.cu", "capi.cpp", "tiling.cpp", "synth.cpp"]
+HEADERS = ["fse_kernels.cuh", "host_internal.hpp"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> Path:
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "tframe_fse.h", Path(__file__)]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    LIBDIR.mkdir(exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = LIBDIR / (src.rsplit(".", 1)[0] + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
+               "-Xptxas", "-v" if verbose else "-O3", "-I", str(ROOT / "include"),
+               "-c", str(CSRC / src), "-o", str(obj)]
+        subprocess.run(cmd, check=True)
+        objs.append(str(obj))
+    tmp = LIB.with_suffix(".so.tmp")
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-ldl"], check=True)
+    os.replace(tmp, LIB)
+    for o in objs:
+        os.remove(o)
+    return LIB
+
+
+def build_oracle(with_ref: bool | None = None) -> None:
+    """Test infrastructure: the C restatement, and the compiled reference shim
+    when /root/reference is present (this container; the GPU box uses the
+    prebuilt oracle/_ref/libtframe_ref.so that travels with the snapshot)."""
+    odir = ROOT / "oracle"
+    subprocess.run(["make", "-s", "-C", str(odir), "liboracle.so"], check=True)
+    ref_inc = Path(os.environ.get("TF_REF_INCLUDE", "/root/reference/proj/include"))
+    if with_ref is None:
+        with_ref = ref_inc.exists()
+    if with_ref:
+        subprocess.run(["make", "-s", "-C", str(odir), "ref", f"REF_INCLUDE={ref_inc}"], check=True)
+
+
+if __name__ == "__main__":
+    build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    if "--oracle" in sys.argv:
+        build_oracle()
+    print(LIB)

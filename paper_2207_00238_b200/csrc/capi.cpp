@@ -1,0 +1,746 @@
+// C-ABI: context, device buffers, launch orchestration and multi-GPU gather.
+//
+// Mirrors the reference master/worker pipeline (runtime.hpp:75-139):
+//   plan (tiling.hpp:99) -> expand (overlap.hpp:25) -> per-tile FSE-lite
+//   (extrapolate.hpp:263) -> crop_core + merge_into (overlap.hpp:52-72)
+// re-designed for B200: tiles of all frames become one table in HBM, an
+// enumeration kernel compacts the blocks that carry an unknown core pixel,
+// one persistent FSE kernel per GPU runs them, and the known pixels plus the
+// FSE output land directly in the output frame (the crop/merge is an index
+// test).  Tiles are spread over GPUs round-robin (runtime.hpp:102); cores are
+// gathered to the root GPU with NCCL send/recv over NVLink.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "fse_kernels.cuh"
+#include "host_internal.hpp"
+
+using tfb::BlockDesc;
+using tfb::BlockStat;
+using tfb::TileDesc;
+
+namespace tfh {
+
+// ------------------------------------------------------------ NCCL (dlopen)
+// NCCL is resolved at run time so that the library shares the process's NCCL
+// (e.g. the one torch already loaded) and loads without it for 1-GPU use.
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      n.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+#define TF_SYM(field, name)                                              \
+  n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name));         \
+  if (!n.field) {                                                        \
+    n.why = std::string("libnccl lacks ") + name;                        \
+    return;                                                              \
+  }
+    TF_SYM(GetUniqueId, "ncclGetUniqueId")
+    TF_SYM(CommInitRank, "ncclCommInitRank")
+    TF_SYM(CommInitAll, "ncclCommInitAll")
+    TF_SYM(CommDestroy, "ncclCommDestroy")
+    TF_SYM(Send, "ncclSend")
+    TF_SYM(Recv, "ncclRecv")
+    TF_SYM(GroupStart, "ncclGroupStart")
+    TF_SYM(GroupEnd, "ncclGroupEnd")
+    TF_SYM(GetErrorString, "ncclGetErrorString")
+#undef TF_SYM
+    n.ok = true;
+  });
+  return n;
+}
+
+// ------------------------------------------------------------ device state
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Gpu {
+  int dev = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_tables = nullptr;
+  DevBuf img, known, out;                       // host-API frame buffers
+  DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv;
+  void* pinned = nullptr;                       // host staging for tables
+  size_t pinned_n = 0;
+  double rho_val = -1.0;
+  int rho_margin = -1;
+  int tw_wmax = 0;
+  int occ[2][tfb::kNumCfgs] = {};
+  int occ_smem[2][tfb::kNumCfgs] = {};
+  ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
+};
+
+}  // namespace tfh
+
+struct tf_ctx {
+  std::vector<tfh::Gpu> gpus;
+  int mode = TF_MODE_EXACT;
+  ncclComm_t rank_comm = nullptr;  // one-process-per-GPU communicator
+  int nranks = 1, rank = 0;
+};
+
+namespace tfh {
+
+#define TF_CUDA(expr)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_error(e_ == cudaErrorMemoryAllocation ? TF_ENOMEM : TF_ECUDA,            \
+                       std::string(#expr) + ": " + cudaGetErrorString(e_));               \
+  } while (0)
+
+#define TF_NCCL(expr)                                                                     \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return set_error(TF_ENCCL, std::string(#expr) + ": " + nccl().GetErrorString(r_));  \
+  } while (0)
+
+static int ensure_pinned(Gpu& g, size_t bytes) {
+  if (g.pinned_n >= bytes) return TF_OK;
+  if (g.pinned) cudaFreeHost(g.pinned);
+  g.pinned = nullptr;
+  g.pinned_n = 0;
+  TF_CUDA(cudaMallocHost(&g.pinned, bytes));
+  g.pinned_n = bytes;
+  return TF_OK;
+}
+
+// Host tables computed exactly as the reference does: rho^d with std::pow
+// (extrapolate.hpp:309) and twiddles (cos, sin)(2*pi*i/n) (extrapolate.hpp:200-207).
+static int upload_tables(Gpu& g, const tf_fse_params& p, int wmax, cudaStream_t s) {
+  const bool rho_ok = g.rho_val == p.rho && g.rho_margin == p.margin;
+  const bool tw_ok = g.tw_wmax >= wmax;
+  if (rho_ok && tw_ok) return TF_OK;
+  const size_t n_rho = static_cast<size_t>(p.margin) + 1;
+  const int tw_n = std::max(wmax, g.tw_wmax);
+  const size_t n_tw = static_cast<size_t>(tw_n) * (tw_n + 1) / 2;  // sizes 1..tw_n
+  std::vector<double> rho(n_rho), tw(2 * n_tw);
+  for (size_t d = 0; d < n_rho; ++d) rho[d] = std::pow(p.rho, static_cast<int>(d));
+  for (int n = 1; n <= tw_n; ++n) {
+    const size_t off = static_cast<size_t>(n) * (n - 1) / 2;
+    for (int i = 0; i < n; ++i) {
+      const double a = 2.0 * std::numbers::pi * i / n;
+      tw[2 * (off + i)] = std::cos(a);
+      tw[2 * (off + i) + 1] = std::sin(a);
+    }
+  }
+  TF_CUDA(g.rho.ensure(n_rho * sizeof(double)));
+  TF_CUDA(g.tw.ensure(tw.size() * sizeof(double)));
+  TF_CUDA(cudaMemcpyAsync(g.rho.p, rho.data(), n_rho * sizeof(double), cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaMemcpyAsync(g.tw.p, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaStreamSynchronize(s));  // pageable sources: keep them alive until copied
+  g.rho_val = p.rho;
+  g.rho_margin = p.margin;
+  g.tw_wmax = tw_n;
+  return TF_OK;
+}
+
+struct Plan {
+  std::vector<tf_rect> cores;
+  std::vector<TileDesc> tiles;  // frames * n_tiles, frame-major
+  int64_t cand_blocks = 0;      // sum gw*gh
+  int max_grid = 0;             // max gw*gh
+  int wmax = 0, nmax = 0;
+  int64_t overhead = 0;
+  int64_t max_core = 0;
+};
+
+static int make_plan(int W, int H, int frames, int n_tiles, int overlap, int B, int margin,
+                     Plan& pl) {
+  if (W < 1 || H < 1 || frames < 1) return set_error(TF_EINVAL, "image dimensions must be >= 1");
+  int rc = plan_proposed(W, H, n_tiles, pl.cores);
+  if (rc != TF_OK) return rc;
+  pl.tiles.clear();
+  int max_hw = 0, max_hh = 0;
+  std::vector<TileDesc> one;
+  for (const tf_rect& c : pl.cores) {
+    tf_rect h;
+    rc = expand(c, overlap, W, H, h);
+    if (rc != TF_OK) return rc;
+    TileDesc t{};
+    t.hx = h.x;
+    t.hy = h.y;
+    t.hw = h.w;
+    t.hh = h.h;
+    t.cx = c.x;
+    t.cy = c.y;
+    t.cw = c.w;
+    t.ch = c.h;
+    t.gw = (h.w + B - 1) / B;
+    t.gh = (h.h + B - 1) / B;
+    if (t.gw > 65535 || t.gh > 65535)
+      return set_error(TF_EUNSUPPORTED, "halo has more than 65535 blocks along one axis");
+    max_hw = std::max(max_hw, h.w);
+    max_hh = std::max(max_hh, h.h);
+    pl.overhead += static_cast<int64_t>(h.w) * h.h - static_cast<int64_t>(c.w) * c.h;
+    pl.max_core = std::max<int64_t>(pl.max_core, static_cast<int64_t>(c.w) * c.h);
+    one.push_back(t);
+  }
+  pl.overhead *= frames;
+  int64_t off = 0;
+  for (int f = 0; f < frames; ++f)
+    for (TileDesc t : one) {
+      t.frame = f;
+      t.grid_off = static_cast<int32_t>(off);
+      off += static_cast<int64_t>(t.gw) * t.gh;
+      pl.max_grid = std::max(pl.max_grid, t.gw * t.gh);
+      pl.tiles.push_back(t);
+    }
+  if (off > (int64_t{1} << 31) - 1) return set_error(TF_EUNSUPPORTED, "too many blocks in one call");
+  pl.cand_blocks = off;
+  const int span = B + 2 * margin;
+  const int mw = std::min(span, max_hw), mh = std::min(span, max_hh);
+  pl.wmax = std::max(mw, mh);
+  pl.nmax = mw * mh;
+  return TF_OK;
+}
+
+struct DevRun {
+  int64_t ref_blocks = 0, processed = 0, iterations = 0, evaluated = 0;
+  double kernel_ms = 0.0, flops = 0.0;
+};
+
+// Enqueue one GPU's share (tiles t % n_parts == part) of a tiled job.
+static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
+                      const uint8_t* d_known, int W, int H, int frames, const tf_fse_params& p,
+                      int part, int n_parts, uint8_t* d_out, cudaStream_t s, bool want_stats,
+                      DevRun* res) {
+  const bool exact = ctx->mode == TF_MODE_EXACT;
+  const int cfg = tfb::pick_config(pl.nmax);
+  if (cfg < 0)
+    return set_error(TF_EUNSUPPORTED, "support window of " + std::to_string(pl.nmax) +
+                                          " bins exceeds the kernel capacity (8192)");
+  const int nt = tfb::kCfgs[cfg].nt, nb = nt * tfb::kCfgs[cfg].bpt;
+  const tfb::SmemLayout lay(nb, pl.wmax, p.iters, nt / 32);
+  if (lay.total > 227 * 1024)
+    return set_error(TF_EUNSUPPORTED, "shared-memory footprint " + std::to_string(lay.total) +
+                                          " B exceeds 227 KB");
+  if (g.occ_smem[exact][cfg] != lay.total) {
+    int occ = 0;
+    TF_CUDA(tfb::fse_prepare(cfg, exact, lay.total, &occ));
+    if (occ < 1) return set_error(TF_EUNSUPPORTED, "FSE kernel cannot be resident");
+    g.occ[exact][cfg] = occ;
+    g.occ_smem[exact][cfg] = lay.total;
+  }
+  int rc = upload_tables(g, p, pl.wmax, s);
+  if (rc != TF_OK) return rc;
+
+  const size_t n_tiles = pl.tiles.size();
+  // table upload through pinned staging; wait for the previous upload first
+  if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
+  rc = ensure_pinned(g, n_tiles * sizeof(TileDesc));
+  if (rc != TF_OK) return rc;
+  std::memcpy(g.pinned, pl.tiles.data(), n_tiles * sizeof(TileDesc));
+  TF_CUDA(g.tiles.ensure(n_tiles * sizeof(TileDesc)));
+  TF_CUDA(g.blocks.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+  TF_CUDA(g.counters.ensure(4 * sizeof(int32_t)));
+  TF_CUDA(g.refblk.ensure(n_tiles * sizeof(unsigned long long)));
+  TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaEventRecord(g.ev_tables, s));
+  TF_CUDA(cudaMemsetAsync(g.counters.p, 0, 4 * sizeof(int32_t), s));
+  TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, n_tiles * sizeof(unsigned long long), s));
+  if (want_stats) {
+    TF_CUDA(g.stats.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
+    TF_CUDA(cudaMemsetAsync(g.stats.p, 0, static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
+  }
+  const size_t frame_bytes = static_cast<size_t>(W) * H * frames;
+  if (d_out != d_img)
+    TF_CUDA(cudaMemcpyAsync(d_out, d_img, frame_bytes, cudaMemcpyDeviceToDevice, s));
+
+  tfb::EnumLaunch e{};
+  e.known = d_known;
+  e.W = W;
+  e.H = H;
+  e.B = p.block;
+  e.tiles = g.tiles.as<TileDesc>();
+  e.n_tiles = static_cast<int32_t>(n_tiles);
+  e.part = part;
+  e.n_parts = n_parts;
+  e.blocks = g.blocks.as<BlockDesc>();
+  e.n_blocks = g.counters.as<int32_t>();
+  e.ref_blocks = g.refblk.as<unsigned long long>();
+  TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
+
+  tfb::FseLaunch a{};
+  a.img = d_img;
+  a.known = d_known;
+  a.out = d_out;
+  a.W = W;
+  a.H = H;
+  a.tiles = g.tiles.as<TileDesc>();
+  a.blocks = g.blocks.as<BlockDesc>();
+  a.n_blocks = g.counters.as<int32_t>();
+  a.next_block = g.counters.as<int32_t>() + 1;
+  a.B = p.block;
+  a.margin = p.margin;
+  a.iters = p.iters;
+  a.gamma = p.gamma;
+  a.rho_pow = g.rho.as<double>();
+  a.tw = g.tw.as<double>();
+  a.wmax = pl.wmax;
+  a.stats = want_stats ? g.stats.as<BlockStat>() : nullptr;
+  int grid = g.sms * g.occ[exact][cfg];
+  if (pl.cand_blocks < grid) grid = static_cast<int>(std::max<int64_t>(1, pl.cand_blocks));
+  TF_CUDA(cudaEventRecord(g.ev0, s));
+  TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
+  TF_CUDA(cudaEventRecord(g.ev1, s));
+
+  if (want_stats && res) {
+    TF_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+    res->kernel_ms = ms;
+    int32_t cnt[4];
+    TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> ref(n_tiles);
+    TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, n_tiles * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost));
+    res->ref_blocks = 0;
+    for (size_t t = 0; t < n_tiles; ++t)
+      if (static_cast<int>(t % n_parts) == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
+    res->processed = cnt[0];
+    std::vector<BlockStat> st(static_cast<size_t>(cnt[0]));
+    if (cnt[0] > 0)
+      TF_CUDA(cudaMemcpy(st.data(), g.stats.p, st.size() * sizeof(BlockStat), cudaMemcpyDeviceToHost));
+    // F_b = 2(4NM + 8NL) + 3N I_b + 8N (I_b + P_b) + 14 U_b T_b
+    double fl = 0.0;
+    for (const BlockStat& b : st) {
+      const double N = static_cast<double>(b.M) * b.L;
+      fl += 2.0 * (4.0 * N * b.M + 8.0 * N * b.L) + 3.0 * N * b.iters +
+            8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
+      res->iterations += b.iters;
+      res->evaluated += b.evaluated;
+    }
+    res->flops = fl;
+  }
+  return TF_OK;
+}
+
+static int select_device(const Gpu& g) {
+  TF_CUDA(cudaSetDevice(g.dev));
+  return TF_OK;
+}
+
+using clk = std::chrono::steady_clock;
+static int64_t us_since(clk::time_point a) {
+  return std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - a).count();
+}
+
+// Core offsets: tile t's core goes to offs[t] inside the payload of its owner
+// (t % n_parts); returns per-owner payload sizes.
+static std::vector<int64_t> core_offsets(const Plan& pl, int n_parts, std::vector<int64_t>& offs) {
+  std::vector<int64_t> size(static_cast<size_t>(n_parts), 0);
+  offs.resize(pl.tiles.size());
+  for (size_t t = 0; t < pl.tiles.size(); ++t) {
+    const int o = static_cast<int>(t % n_parts);
+    offs[t] = size[o];
+    size[o] += static_cast<int64_t>(pl.tiles[t].cw) * pl.tiles[t].ch;
+  }
+  return size;
+}
+
+}  // namespace tfh
+
+using namespace tfh;
+
+extern "C" {
+
+const char* tf_last_error(const tf_ctx*) { return g_last_error.c_str(); }
+
+int tf_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) n = 0;
+  if (out) *out = n;
+  return e == cudaSuccess ? TF_OK : set_error(TF_ECUDA, cudaGetErrorString(e));
+}
+
+tf_ctx* tf_create(int n_gpus, const int* device_ids) {
+  if (n_gpus < 1) {
+    set_error(TF_EINVAL, "tf_create: n_gpus must be >= 1");
+    return nullptr;
+  }
+  int have = 0;
+  cudaError_t e = cudaGetDeviceCount(&have);
+  if (e != cudaSuccess || have < 1) {
+    set_error(TF_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  auto ctx = std::make_unique<tf_ctx>();
+  ctx->gpus.resize(static_cast<size_t>(n_gpus));
+  for (int i = 0; i < n_gpus; ++i) {
+    Gpu& g = ctx->gpus[static_cast<size_t>(i)];
+    g.dev = device_ids ? device_ids[i] : i;
+    if (g.dev < 0 || g.dev >= have) {
+      set_error(TF_EINVAL, "tf_create: device id " + std::to_string(g.dev) + " out of range");
+      return nullptr;
+    }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, g.dev) != cudaSuccess || prop.major < 10) {
+      set_error(TF_ECUDA, "tf_create: device " + std::to_string(g.dev) +
+                              " is not an sm_100 (Blackwell) GPU");
+      return nullptr;
+    }
+    g.sms = prop.multiProcessorCount;
+    if (cudaSetDevice(g.dev) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&g.ev0) != cudaSuccess || cudaEventCreate(&g.ev1) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g.ev_tables, cudaEventDisableTiming) != cudaSuccess) {
+      set_error(TF_ECUDA, "tf_create: stream/event creation failed");
+      return nullptr;
+    }
+  }
+  return ctx.release();
+}
+
+void tf_destroy(tf_ctx* ctx) {
+  if (!ctx) return;
+  for (Gpu& g : ctx->gpus) {
+    cudaSetDevice(g.dev);
+    if (g.stream) cudaStreamSynchronize(g.stream);
+    if (g.comm && nccl().ok) nccl().CommDestroy(g.comm);
+    for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
+                      &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv})
+      b->release();
+    if (g.pinned) cudaFreeHost(g.pinned);
+    if (g.ev0) cudaEventDestroy(g.ev0);
+    if (g.ev1) cudaEventDestroy(g.ev1);
+    if (g.ev_tables) cudaEventDestroy(g.ev_tables);
+    if (g.stream) cudaStreamDestroy(g.stream);
+  }
+  if (ctx->rank_comm && nccl().ok) nccl().CommDestroy(ctx->rank_comm);
+  delete ctx;
+}
+
+int tf_set_mode(tf_ctx* ctx, int mode) {
+  if (!ctx) return set_error(TF_EINVAL, "null context");
+  if (mode != TF_MODE_EXACT && mode != TF_MODE_FAST) return set_error(TF_EINVAL, "bad mode");
+  ctx->mode = mode;
+  return TF_OK;
+}
+
+int tf_get_mode(const tf_ctx* ctx) { return ctx ? ctx->mode : -1; }
+
+int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, const uint8_t* d_known,
+                                int W, int H, int frames, int tiles, int overlap,
+                                const tf_fse_params* p, int part, int n_parts, uint8_t* d_out,
+                                void* stream, tf_run_stats* stats) {
+  if (!ctx || gpu < 0 || gpu >= static_cast<int>(ctx->gpus.size()))
+    return set_error(TF_EINVAL, "bad context or gpu index");
+  int rc = check_params(p);
+  if (rc != TF_OK) return rc;
+  if (!d_img || !d_known || !d_out) return set_error(TF_EINVAL, "null buffer");
+  if (n_parts < 1 || part < 0 || part >= n_parts) return set_error(TF_EINVAL, "bad part/n_parts");
+  Gpu& g = ctx->gpus[static_cast<size_t>(gpu)];
+  rc = select_device(g);
+  if (rc != TF_OK) return rc;
+  const auto t0 = clk::now();
+  Plan pl;
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
+  if (rc != TF_OK) return rc;
+  const int64_t plan_us = us_since(t0);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  DevRun dr;
+  rc = run_device(ctx, g, pl, d_img, d_known, W, H, frames, *p, part, n_parts, d_out, s,
+                  stats != nullptr, &dr);
+  if (rc != TF_OK) return rc;
+  if (stats) {
+    *stats = tf_run_stats{};
+    stats->plan_us = plan_us;
+    stats->total_us = us_since(t0);
+    stats->overhead_pixels = pl.overhead;
+    stats->blocks_reference = dr.ref_blocks;
+    stats->blocks_processed = dr.processed;
+    stats->kernel_ms = dr.kernel_ms;
+    stats->flops = dr.flops;
+    stats->iterations = dr.iterations;
+    stats->pixels_evaluated = dr.evaluated;
+  }
+  return TF_OK;
+}
+
+int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                         int frames, int tiles, int overlap, const tf_fse_params* p, uint8_t* out,
+                         tf_run_stats* stats) {
+  if (!ctx) return set_error(TF_EINVAL, "null context");
+  if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
+  int rc = check_params(p);
+  if (rc != TF_OK) return rc;
+  const auto t0 = clk::now();
+  Plan pl;
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
+  if (rc != TF_OK) return rc;
+  const int64_t plan_us = us_since(t0);
+  const int n = static_cast<int>(ctx->gpus.size());
+  const size_t bytes = static_cast<size_t>(W) * H * frames;
+  // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
+  std::vector<DevRun> dr(static_cast<size_t>(n));
+  for (int gi = 0; gi < n; ++gi) {
+    Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+    rc = select_device(g);
+    if (rc != TF_OK) return rc;
+    TF_CUDA(g.img.ensure(bytes));
+    TF_CUDA(g.known.ensure(bytes));
+    TF_CUDA(g.out.ensure(bytes));
+    TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
+    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+    rc = run_device(ctx, g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, *p, gi,
+                    n, g.out.as<uint8_t>(), g.stream, false, nullptr);
+    if (rc != TF_OK) return rc;
+  }
+  const auto t_dispatched = clk::now();
+  const int64_t distribute_us = us_since(t0) - plan_us;
+  // ---- gather the cores of GPUs 1..n-1 into GPU 0 (NCCL send/recv over NVLink)
+  Gpu& root = ctx->gpus[0];
+  if (n > 1) {
+    Nccl& nc = nccl();
+    if (!nc.ok) return set_error(TF_ENCCL, nc.why);
+    if (!root.comm) {
+      std::vector<ncclComm_t> comms(static_cast<size_t>(n));
+      std::vector<int> devs;
+      for (const Gpu& g : ctx->gpus) devs.push_back(g.dev);
+      TF_NCCL(nc.CommInitAll(comms.data(), n, devs.data()));
+      for (int gi = 0; gi < n; ++gi) ctx->gpus[static_cast<size_t>(gi)].comm = comms[static_cast<size_t>(gi)];
+    }
+    std::vector<int64_t> offs;
+    const std::vector<int64_t> size = core_offsets(pl, n, offs);
+    int64_t total = 0;
+    std::vector<int64_t> base(static_cast<size_t>(n), 0);
+    for (int gi = 1; gi < n; ++gi) {
+      base[static_cast<size_t>(gi)] = total;
+      total += size[static_cast<size_t>(gi)];
+    }
+    for (int gi = 0; gi < n; ++gi) {
+      Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+      rc = select_device(g);
+      if (rc != TF_OK) return rc;
+      TF_CUDA(g.offs.ensure(offs.size() * sizeof(int64_t)));
+      TF_CUDA(cudaMemcpyAsync(g.offs.p, offs.data(), offs.size() * sizeof(int64_t),
+                              cudaMemcpyHostToDevice, g.stream));
+      if (gi > 0) {
+        TF_CUDA(g.packed.ensure(static_cast<size_t>(size[static_cast<size_t>(gi)])));
+        TF_CUDA(tfb::cores_launch(g.out.as<uint8_t>(), W, H, g.tiles.as<TileDesc>(),
+                                  static_cast<int>(pl.tiles.size()), gi, n, g.offs.as<int64_t>(),
+                                  g.packed.as<uint8_t>(), false, pl.max_core, g.stream));
+      }
+    }
+    TF_CUDA(cudaSetDevice(root.dev));
+    TF_CUDA(root.recv.ensure(static_cast<size_t>(std::max<int64_t>(total, 1))));
+    TF_NCCL(nc.GroupStart());
+    for (int gi = 1; gi < n; ++gi) {
+      Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+      const size_t sz = static_cast<size_t>(size[static_cast<size_t>(gi)]);
+      if (!sz) continue;
+      TF_NCCL(nc.Send(g.packed.p, sz, ncclUint8, 0, g.comm, g.stream));
+      TF_NCCL(nc.Recv(root.recv.as<uint8_t>() + base[static_cast<size_t>(gi)], sz, ncclUint8, gi,
+                      root.comm, root.stream));
+    }
+    TF_NCCL(nc.GroupEnd());
+    TF_CUDA(cudaSetDevice(root.dev));
+    for (int gi = 1; gi < n; ++gi)
+      TF_CUDA(tfb::cores_launch(root.out.as<uint8_t>(), W, H, root.tiles.as<TileDesc>(),
+                                static_cast<int>(pl.tiles.size()), gi, n, root.offs.as<int64_t>(),
+                                root.recv.as<uint8_t>() + base[static_cast<size_t>(gi)], true,
+                                pl.max_core, root.stream));
+  }
+  TF_CUDA(cudaSetDevice(root.dev));
+  TF_CUDA(cudaMemcpyAsync(out, root.out.p, bytes, cudaMemcpyDeviceToHost, root.stream));
+  TF_CUDA(cudaStreamSynchronize(root.stream));
+  for (int gi = 1; gi < n; ++gi) {
+    TF_CUDA(cudaSetDevice(ctx->gpus[static_cast<size_t>(gi)].dev));
+    TF_CUDA(cudaStreamSynchronize(ctx->gpus[static_cast<size_t>(gi)].stream));
+  }
+  if (stats) {
+    *stats = tf_run_stats{};
+    stats->plan_us = plan_us;
+    stats->distribute_us = distribute_us;
+    stats->compute_span_us = std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t_dispatched).count();
+    stats->total_us = us_since(t0);
+    stats->overhead_pixels = pl.overhead;
+    double kms = 0.0;
+    for (int gi = 0; gi < n; ++gi) {
+      Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+      TF_CUDA(cudaSetDevice(g.dev));
+      float ms = 0.f;
+      TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+      kms = std::max(kms, static_cast<double>(ms));
+      int32_t cnt[4];
+      TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+      stats->blocks_processed += cnt[0];
+      std::vector<unsigned long long> ref(pl.tiles.size());
+      TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+      for (size_t t = 0; t < ref.size(); ++t)
+        if (static_cast<int>(t % n) == gi) stats->blocks_reference += static_cast<int64_t>(ref[t]);
+    }
+    stats->kernel_ms = kms;
+  }
+  return TF_OK;
+}
+
+int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int w, int h,
+                       const tf_fse_params* p, uint8_t* out) {
+  // one tile, no overlap: the whole image is the halo (extrapolate.hpp:263)
+  return tf_tiled_extrapolate(ctx, img, known, w, h, 1, 1, 0, p, out, nullptr);
+}
+
+// ---- one process per GPU ---------------------------------------------------
+int tf_comm_unique_id(uint8_t id[128]) {
+  Nccl& nc = nccl();
+  if (!nc.ok) return set_error(TF_ENCCL, nc.why);
+  ncclUniqueId u;
+  TF_NCCL(nc.GetUniqueId(&u));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return TF_OK;
+}
+
+int tf_comm_init(tf_ctx* ctx, int nranks, int rank, const uint8_t id[128]) {
+  if (!ctx || ctx->gpus.size() != 1) return set_error(TF_EINVAL, "tf_comm_init needs a 1-GPU context");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(TF_EINVAL, "bad rank/nranks");
+  Nccl& nc = nccl();
+  if (!nc.ok) return set_error(TF_ENCCL, nc.why);
+  TF_CUDA(cudaSetDevice(ctx->gpus[0].dev));
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  if (ctx->rank_comm) nc.CommDestroy(ctx->rank_comm);
+  ctx->rank_comm = nullptr;
+  TF_NCCL(nc.CommInitRank(&ctx->rank_comm, nranks, u, rank));
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return TF_OK;
+}
+
+int tf_comm_gather(tf_ctx* ctx, const void* d_send, void* d_recv, int64_t bytes, int root,
+                   void* stream) {
+  if (!ctx || !ctx->rank_comm) return set_error(TF_EINVAL, "no communicator (tf_comm_init)");
+  if (root < 0 || root >= ctx->nranks || bytes < 0) return set_error(TF_EINVAL, "bad root/bytes");
+  Nccl& nc = nccl();
+  Gpu& g = ctx->gpus[0];
+  TF_CUDA(cudaSetDevice(g.dev));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  const size_t sz = static_cast<size_t>(bytes);
+  if (ctx->rank == root) {
+    if (!d_recv) return set_error(TF_EINVAL, "root needs a receive buffer");
+    uint8_t* r = static_cast<uint8_t*>(d_recv);
+    TF_CUDA(cudaMemcpyAsync(r + sz * root, d_send, sz, cudaMemcpyDeviceToDevice, s));
+    TF_NCCL(nc.GroupStart());
+    for (int q = 0; q < ctx->nranks; ++q)
+      if (q != root) TF_NCCL(nc.Recv(r + sz * q, sz, ncclUint8, q, ctx->rank_comm, s));
+    TF_NCCL(nc.GroupEnd());
+  } else {
+    TF_NCCL(nc.Send(d_send, sz, ncclUint8, root, ctx->rank_comm, s));
+  }
+  return TF_OK;
+}
+
+int tf_comm_gather_cores(tf_ctx* ctx, uint8_t* d_out, int W, int H, int frames, int tiles,
+                         int root, void* stream) {
+  if (!ctx || !ctx->rank_comm) return set_error(TF_EINVAL, "no communicator (tf_comm_init)");
+  Plan pl;
+  int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl);
+  if (rc != TF_OK) return rc;
+  Nccl& nc = nccl();
+  Gpu& g = ctx->gpus[0];
+  TF_CUDA(cudaSetDevice(g.dev));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  const int n = ctx->nranks;
+  std::vector<int64_t> offs;
+  const std::vector<int64_t> size = core_offsets(pl, n, offs);
+  if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
+  const size_t tb = pl.tiles.size() * sizeof(TileDesc), ob = offs.size() * sizeof(int64_t);
+  rc = ensure_pinned(g, tb + ob);
+  if (rc != TF_OK) return rc;
+  std::memcpy(g.pinned, pl.tiles.data(), tb);
+  std::memcpy(static_cast<uint8_t*>(g.pinned) + tb, offs.data(), ob);
+  TF_CUDA(g.tiles.ensure(tb));
+  TF_CUDA(g.offs.ensure(ob));
+  TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, tb, cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaMemcpyAsync(g.offs.p, static_cast<uint8_t*>(g.pinned) + tb, ob, cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaEventRecord(g.ev_tables, s));
+  const int nt = static_cast<int>(pl.tiles.size());
+  if (ctx->rank == root) {
+    int64_t total = 0;
+    std::vector<int64_t> base(static_cast<size_t>(n), 0);
+    for (int q = 0; q < n; ++q)
+      if (q != root) {
+        base[static_cast<size_t>(q)] = total;
+        total += size[static_cast<size_t>(q)];
+      }
+    TF_CUDA(g.recv.ensure(static_cast<size_t>(std::max<int64_t>(total, 1))));
+    TF_NCCL(nc.GroupStart());
+    for (int q = 0; q < n; ++q)
+      if (q != root && size[static_cast<size_t>(q)])
+        TF_NCCL(nc.Recv(g.recv.as<uint8_t>() + base[static_cast<size_t>(q)],
+                        static_cast<size_t>(size[static_cast<size_t>(q)]), ncclUint8, q,
+                        ctx->rank_comm, s));
+    TF_NCCL(nc.GroupEnd());
+    for (int q = 0; q < n; ++q)
+      if (q != root)
+        TF_CUDA(tfb::cores_launch(d_out, W, H, g.tiles.as<TileDesc>(), nt, q, n, g.offs.as<int64_t>(),
+                                  g.recv.as<uint8_t>() + base[static_cast<size_t>(q)], true,
+                                  pl.max_core, s));
+  } else {
+    const size_t sz = static_cast<size_t>(size[static_cast<size_t>(ctx->rank)]);
+    TF_CUDA(g.packed.ensure(std::max<size_t>(sz, 1)));
+    TF_CUDA(tfb::cores_launch(d_out, W, H, g.tiles.as<TileDesc>(), nt, ctx->rank, n,
+                              g.offs.as<int64_t>(), g.packed.as<uint8_t>(), false, pl.max_core, s));
+    if (sz) TF_NCCL(nc.Send(g.packed.p, sz, ncclUint8, root, ctx->rank_comm, s));
+  }
+  return TF_OK;
+}
+
+}  // extern "C"

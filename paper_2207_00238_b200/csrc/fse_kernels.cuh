@@ -1,0 +1,105 @@
+// Device-side data layout shared by the host launcher and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tfb {
+
+// One (frame, tile) unit: halo and core rects in absolute frame coordinates.
+// The FSE block grid is anchored at the halo origin (extrapolate.hpp:278-279
+// run on the extracted halo, runtime.hpp:98).
+struct TileDesc {
+  int32_t frame;
+  int32_t hx, hy, hw, hh;  // halo (overlap.hpp:25-34)
+  int32_t cx, cy, cw, ch;  // core
+  int32_t gw, gh;          // block-grid dims: ceil(hw/B), ceil(hh/B)
+  int32_t grid_off;        // prefix sum of gw*gh over previous tiles
+};
+
+// One processed block: tile index + block-grid coordinates.
+struct BlockDesc {
+  uint32_t tile;
+  uint16_t bxi, byi;
+};
+
+// Per-block counters (SURVEY §8(d) F_b terms), written by the FSE kernel.
+struct BlockStat {
+  int32_t M, L;      // support window = DFT size
+  int32_t iters;     // executed iterations I_b
+  int32_t pairs;     // non-self-conjugate selections P_b
+  int32_t touched;   // touched bins T_b
+  int32_t evaluated; // unknown core pixels evaluated (U_b restricted to the core)
+};
+
+struct FseLaunch {
+  const uint8_t* img;
+  const uint8_t* known;
+  uint8_t* out;
+  int32_t W, H;  // frame dims, row stride W, plane W*H
+  const TileDesc* tiles;
+  const BlockDesc* blocks;
+  const int32_t* n_blocks;  // device counter written by the enumerator
+  int32_t* next_block;      // work-queue head (zeroed before launch)
+  int32_t B, margin, iters;
+  double gamma;
+  const double* rho_pow;  // rho^d, d = 0..margin (host std::pow, extrapolate.hpp:309)
+  const double* tw;       // twiddles (cos,sin) interleaved, sizes n=1..wmax at n*(n-1)/2
+  int32_t wmax;           // max window side in this launch
+  BlockStat* stats;       // optional
+};
+
+struct EnumLaunch {
+  const uint8_t* known;
+  int32_t W, H, B;
+  const TileDesc* tiles;
+  int32_t n_tiles;
+  int32_t part, n_parts;      // only tiles t % n_parts == part are enqueued
+  BlockDesc* blocks;          // out
+  int32_t* n_blocks;          // out: processed-block count
+  unsigned long long* ref_blocks;  // out, per tile: blocks the reference processes
+};
+
+constexpr int kCY = 4;  // rows per DFT chunk
+
+// Shared-memory layout of the FSE kernel (bytes), computed identically on host and device.
+//   [pad][W spectrum: double2 x nb][pad][twiddles: double2 x 2*wmax][union][slots][misc]
+//   union = DFT phase {cw, cwv: double x kCY*wmax; rw, rr: double2 x kCY*wmax; pix, kn: u8 x nb}
+//         | loop phase {mval: double2 x cap; lst: int32 x cap; pos: int16 x nb}
+struct SmemLayout {
+  int nb, wmax, iters, nw, cap;
+  int off_w, off_tw, off_union, off_pix, off_kn, off_lst, off_pos, off_slots, off_misc, total;
+  __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
+  __host__ __device__ SmemLayout(int nb_, int wmax_, int iters_, int nw_)
+      : nb(nb_), wmax(wmax_), iters(iters_), nw(nw_) {
+    cap = iters >= (nb + 1) / 2 ? nb : 2 * iters;  // touched bins are distinct: <= min(2I, N)
+    off_w = 16 * wmax;                  // W padded by wmax entries on both sides
+    off_tw = off_w + 16 * (nb + wmax);
+    off_union = off_tw + align16(2 * 16 * wmax);
+    off_pix = off_union + 48 * kCY * wmax;
+    off_kn = off_pix + nb;
+    const int dft_end = off_kn + nb;
+    off_lst = off_union + 16 * cap;
+    off_pos = off_lst + 4 * cap;
+    const int loop_end = off_pos + 2 * nb;
+    off_slots = align16(dft_end > loop_end ? dft_end : loop_end);
+    off_misc = off_slots + 2 * nw * 32;
+    total = off_misc + 16;
+  }
+};
+
+// ---- launch helpers (fse_kernels.cu)
+struct KernelCfg {
+  int nt, bpt;
+};
+constexpr int kNumCfgs = 7;
+extern const KernelCfg kCfgs[kNumCfgs];
+int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
+cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
+                       cudaStream_t s);
+cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
+cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
+                         int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,
+                         int64_t max_core, cudaStream_t s);
+
+}  // namespace tfb
