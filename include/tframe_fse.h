@@ -147,6 +147,15 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img,
                                 int overlap, const tf_fse_params* p, int part, int n_parts,
                                 uint8_t* d_out, void* stream, tf_run_stats* stats);
 
+/* ---- measurement ----------------------------------------------------------- */
+/* Device durations (ms) of the most recent FSE kernel launches on GPU `gpu`
+ * (oldest first, up to max_n; the context keeps the last 256).  Synchronises
+ * the GPU's pending FSE launches.  Returns the count written, or -status. */
+int tf_fse_kernel_times(tf_ctx* ctx, int gpu, float* out_ms, int max_n);
+/* FP64 DFMA peak (TFLOP/s) and shared-memory LDS.128 bandwidth (TB/s) of a
+ * device, measured with calibration kernels (roofline denominators). */
+int tf_calibrate(int device, double* fp64_tflops, double* smem_tbs);
+
 /* ---- multi-rank (one process per GPU, NCCL over NVLink) ------------------ */
 /* 128-byte NCCL unique id, to be broadcast by the caller's bootstrap. */
 int tf_comm_unique_id(uint8_t id[128]);
@@ -156,6 +165,12 @@ int tf_comm_init(tf_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
  * nranks*bytes); non-root ranks may pass d_recv = NULL. */
 int tf_comm_gather(tf_ctx* ctx, const void* d_send, void* d_recv, int64_t bytes, int root,
                    void* stream);
+/* Host-side layout of the core gather (no GPU needed): for the frames*tiles
+ * units (frame-major) gives each core rect, its frame, its owner part
+ * (t % n_parts, runtime.hpp:102) and its byte offset inside the owner's packed
+ * payload; part_bytes[n_parts] receives each payload size. Any output may be NULL. */
+int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* cores,
+                   int32_t* frame_of, int32_t* owner, int64_t* offs, int64_t* part_bytes);
 /* Gather the cores of tiles owned by each rank (t % nranks == rank) from every
  * rank's d_img-sized buffer into root's d_out (same layout).  Packs, gathers
  * and unpacks on device. */

@@ -270,3 +270,8 @@ def psnr(a, b) -> float:
     d = a.astype(np.float64) - b.astype(np.float64)
     mse = float(np.mean(d * d))
     return float("inf") if mse == 0.0 else 10.0 * np.log10(255.0 * 255.0 / mse)
+
+
+def ref_interior_boundary(W, H, N) -> int:
+    """tiling.hpp:231 on plan_proposed(W, H, N), via the compiled reference."""
+    return int(ref().ref_interior_boundary(W, H, N))

@@ -60,10 +60,13 @@ SIGNATURES = {
     "tf_tiled_extrapolate_device": (_i, [_vp, _i, _vp, _vp, _i, _i, _i, _i, _i,
                                          C.POINTER(tf_fse_params), _i, _i, _vp, _vp,
                                          C.POINTER(tf_run_stats)]),
+    "tf_fse_kernel_times": (_i, [_vp, _i, C.POINTER(C.c_float), _i]),
+    "tf_calibrate": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tf_comm_unique_id": (_i, [_vp]),
     "tf_comm_init": (_i, [_vp, _i, _i, _vp]),
     "tf_comm_gather": (_i, [_vp, _vp, _vp, C.c_int64, _i, _vp]),
     "tf_comm_gather_cores": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "tf_core_layout": (_i, [_i, _i, _i, _i, _i, C.POINTER(tf_rect), _vp, _vp, _vp, _vp]),
     "tf_synth_frame": (_i, [_i, _i, _i, _i, _vp, _vp]),
 }
 

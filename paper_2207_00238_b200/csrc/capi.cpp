@@ -120,6 +120,10 @@ struct Gpu {
   int occ[2][tfb::kNumCfgs] = {};
   int occ_smem[2][tfb::kNumCfgs] = {};
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
+  // ring of (start, stop) events around the most recent FSE kernel launches
+  static constexpr int kRing = 256;
+  cudaEvent_t ring0[kRing] = {}, ring1[kRing] = {};
+  int64_t launches = 0;
 };
 
 }  // namespace tfh
@@ -334,9 +338,17 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   a.stats = want_stats ? g.stats.as<BlockStat>() : nullptr;
   int grid = g.sms * g.occ[exact][cfg];
   if (pl.cand_blocks < grid) grid = static_cast<int>(std::max<int64_t>(1, pl.cand_blocks));
+  const int slot = static_cast<int>(g.launches % Gpu::kRing);
+  if (!g.ring0[slot]) {
+    TF_CUDA(cudaEventCreate(&g.ring0[slot]));
+    TF_CUDA(cudaEventCreate(&g.ring1[slot]));
+  }
   TF_CUDA(cudaEventRecord(g.ev0, s));
+  TF_CUDA(cudaEventRecord(g.ring0[slot], s));
   TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
+  TF_CUDA(cudaEventRecord(g.ring1[slot], s));
   TF_CUDA(cudaEventRecord(g.ev1, s));
+  ++g.launches;
 
   if (want_stats && res) {
     TF_CUDA(cudaStreamSynchronize(s));
@@ -456,6 +468,10 @@ void tf_destroy(tf_ctx* ctx) {
                       &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv})
       b->release();
     if (g.pinned) cudaFreeHost(g.pinned);
+    for (int r = 0; r < Gpu::kRing; ++r) {
+      if (g.ring0[r]) cudaEventDestroy(g.ring0[r]);
+      if (g.ring1[r]) cudaEventDestroy(g.ring1[r]);
+    }
     if (g.ev0) cudaEventDestroy(g.ev0);
     if (g.ev1) cudaEventDestroy(g.ev1);
     if (g.ev_tables) cudaEventDestroy(g.ev_tables);
@@ -635,6 +651,41 @@ int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
                        const tf_fse_params* p, uint8_t* out) {
   // one tile, no overlap: the whole image is the halo (extrapolate.hpp:263)
   return tf_tiled_extrapolate(ctx, img, known, w, h, 1, 1, 0, p, out, nullptr);
+}
+
+int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* cores,
+                   int32_t* frame_of, int32_t* owner, int64_t* offs, int64_t* part_bytes) {
+  if (n_parts < 1) return set_error(TF_EINVAL, "n_parts must be >= 1");
+  Plan pl;
+  const int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl);
+  if (rc != TF_OK) return rc;
+  std::vector<int64_t> o;
+  const std::vector<int64_t> size = core_offsets(pl, n_parts, o);
+  for (size_t t = 0; t < pl.tiles.size(); ++t) {
+    const TileDesc& d = pl.tiles[t];
+    if (cores) cores[t] = tf_rect{d.cx, d.cy, d.cw, d.ch};
+    if (frame_of) frame_of[t] = d.frame;
+    if (owner) owner[t] = static_cast<int32_t>(t % static_cast<size_t>(n_parts));
+    if (offs) offs[t] = o[t];
+  }
+  if (part_bytes) std::copy(size.begin(), size.end(), part_bytes);
+  return TF_OK;
+}
+
+int tf_fse_kernel_times(tf_ctx* ctx, int gpu, float* out_ms, int max_n) {
+  if (!ctx || gpu < 0 || gpu >= static_cast<int>(ctx->gpus.size()) || !out_ms || max_n < 0)
+    return -set_error(TF_EINVAL, "bad arguments");
+  Gpu& g = ctx->gpus[static_cast<size_t>(gpu)];
+  if (cudaSetDevice(g.dev) != cudaSuccess) return -set_error(TF_ECUDA, "cudaSetDevice");
+  const int64_t have = std::min<int64_t>(g.launches, Gpu::kRing);
+  const int n = static_cast<int>(std::min<int64_t>(have, max_n));
+  for (int q = 0; q < n; ++q) {
+    const int slot = static_cast<int>((g.launches - n + q) % Gpu::kRing);
+    cudaError_t e = cudaEventSynchronize(g.ring1[slot]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&out_ms[q], g.ring0[slot], g.ring1[slot]);
+    if (e != cudaSuccess) return -set_error(TF_ECUDA, cudaGetErrorString(e));
+  }
+  return n;
 }
 
 // ---- one process per GPU ---------------------------------------------------

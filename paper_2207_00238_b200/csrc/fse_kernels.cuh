@@ -62,18 +62,17 @@ struct EnumLaunch {
 constexpr int kCY = 4;  // rows per DFT chunk
 
 // Shared-memory layout of the FSE kernel (bytes), computed identically on host and device.
-//   [pad][W spectrum: double2 x nb][pad][twiddles: double2 x 2*wmax][union][slots][misc]
+//   [W replicated along k: double2 x L x 2M <= 2*nb][twiddles: double2 x 2*wmax][union][slots][misc]
 //   union = DFT phase {cw, cwv: double x kCY*wmax; rw, rr: double2 x kCY*wmax; pix, kn: u8 x nb}
 //         | loop phase {mval: double2 x cap; lst: int32 x cap; pos: int16 x nb}
 struct SmemLayout {
   int nb, wmax, iters, nw, cap;
-  int off_w, off_tw, off_union, off_pix, off_kn, off_lst, off_pos, off_slots, off_misc, total;
+  int off_tw, off_union, off_pix, off_kn, off_lst, off_pos, off_slots, off_misc, total;
   __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
   __host__ __device__ SmemLayout(int nb_, int wmax_, int iters_, int nw_)
       : nb(nb_), wmax(wmax_), iters(iters_), nw(nw_) {
     cap = iters >= (nb + 1) / 2 ? nb : 2 * iters;  // touched bins are distinct: <= min(2I, N)
-    off_w = 16 * wmax;                  // W padded by wmax entries on both sides
-    off_tw = off_w + 16 * (nb + wmax);
+    off_tw = 32 * nb;
     off_union = off_tw + align16(2 * 16 * wmax);
     off_pix = off_union + 48 * kCY * wmax;
     off_kn = off_pix + nb;
@@ -91,7 +90,7 @@ struct SmemLayout {
 struct KernelCfg {
   int nt, bpt;
 };
-constexpr int kNumCfgs = 7;
+constexpr int kNumCfgs = 9;
 extern const KernelCfg kCfgs[kNumCfgs];
 int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
