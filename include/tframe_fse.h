@@ -155,6 +155,9 @@ int tf_fse_kernel_times(tf_ctx* ctx, int gpu, float* out_ms, int max_n);
 /* FP64 DFMA peak (TFLOP/s) and shared-memory LDS.128 bandwidth (TB/s) of a
  * device, measured with calibration kernels (roofline denominators). */
 int tf_calibrate(int device, double* fp64_tflops, double* smem_tbs);
+/* Self-test: the FSE kernel's hoisted-reciprocal division must be bit-identical
+ * to IEEE a/b; counts mismatches over n hashed operand pairs (expect 0). */
+int tf_selftest_div(int device, int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ---- multi-rank (one process per GPU, NCCL over NVLink) ------------------ */
 /* 128-byte NCCL unique id, to be broadcast by the caller's bootstrap. */

@@ -8,7 +8,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtframe_b200.so"
+import os
+
+# TF_LIB selects a tuning variant built by `build.py --variant` (default: the product library)
+LIB_PATH = Path(os.environ.get("TF_LIB") or Path(__file__).resolve().parent / "_lib" / "libtframe_b200.so")
 HEADER = Path(__file__).resolve().parent.parent / "include" / "tframe_fse.h"
 
 TF_OK, TF_EINVAL, TF_EIO, TF_EPROTO, TF_ETILING, TF_ECUDA, TF_ENCCL, TF_ENOMEM, TF_EUNSUPPORTED = range(9)
@@ -62,6 +65,7 @@ SIGNATURES = {
                                          C.POINTER(tf_run_stats)]),
     "tf_fse_kernel_times": (_i, [_vp, _i, C.POINTER(C.c_float), _i]),
     "tf_calibrate": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tf_selftest_div": (_i, [_i, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     "tf_comm_unique_id": (_i, [_vp]),
     "tf_comm_init": (_i, [_vp, _i, _i, _vp]),
     "tf_comm_gather": (_i, [_vp, _vp, _vp, C.c_int64, _i, _vp]),

@@ -31,25 +31,29 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> Path:
+def build_lib(force: bool = False, verbose: bool = False, out: Path | None = None,
+              defines: tuple[str, ...] = ()) -> Path:
+    """Build libtframe_b200.so (or a tuning variant at `out` with extra -D defines)."""
+    target = out or LIB
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "tframe_fse.h", Path(__file__)]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    LIBDIR.mkdir(exist_ok=True)
+    if not force and not _stale(target, deps):
+        return target
+    target.parent.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = LIBDIR / (src.rsplit(".", 1)[0] + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
+        obj = target.parent / (target.stem + "." + src.rsplit(".", 1)[0] + ".o")
+        cmd = [NVCC, *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "-I", str(ROOT / "include"),
                "-c", str(CSRC / src), "-o", str(obj)]
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    target.parent.mkdir(parents=True, exist_ok=True)
+    tmp = target.with_suffix(".so.tmp")
     subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-ldl"], check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     for o in objs:
         os.remove(o)
-    return LIB
+    return target
 
 
 def build_oracle(with_ref: bool | None = None) -> None:
@@ -66,6 +70,11 @@ def build_oracle(with_ref: bool | None = None) -> None:
 
 
 if __name__ == "__main__":
+    if "--variant" in sys.argv:  # --variant NAME DEF1 DEF2 ... (tuning builds under _lib/variants/)
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], tuple(sys.argv[i + 2:])
+        print(build_lib(force=True, out=LIBDIR / "variants" / f"{name}.so", defines=defs))
+        sys.exit(0)
     build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
     if "--oracle" in sys.argv:
         build_oracle()

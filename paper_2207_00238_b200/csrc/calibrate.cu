@@ -3,6 +3,7 @@
 // device (the FSE kernel is FP64/shared-memory bound, not HBM/tensor bound).
 #include <cuda_runtime.h>
 
+#include "fse_kernels.cuh"
 #include "host_internal.hpp"
 
 namespace {
@@ -81,5 +82,23 @@ extern "C" int tf_calibrate(int device, double* fp64_tflops, double* smem_tbs) {
   if (e != cudaSuccess) return tfh::set_error(TF_ECUDA, cudaGetErrorString(e));
   if (fp64_tflops) *fp64_tflops = best_fma / 1e12;
   if (smem_tbs) *smem_tbs = best_lds / 1e12;
+  return TF_OK;
+}
+
+// Exactness self-test of the kernel's hoisted-reciprocal division (div_rn)
+// against __ddiv_rn on n hashed operand pairs; *mismatches must be 0.
+extern "C" int tf_selftest_div(int device, int64_t n, uint64_t seed, int64_t* mismatches) {
+  if (!mismatches || n < 0) return tfh::set_error(TF_EINVAL, "bad arguments");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return tfh::set_error(TF_ECUDA, cudaGetErrorString(e));
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return tfh::set_error(TF_ENOMEM, "selftest alloc");
+  cudaMemset(d, 0, sizeof(*d));
+  e = tfb::div_selftest_launch(n, seed, d, nullptr);
+  unsigned long long bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&bad, d, sizeof(bad), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return tfh::set_error(TF_ECUDA, cudaGetErrorString(e));
+  *mismatches = static_cast<int64_t>(bad);
   return TF_OK;
 }

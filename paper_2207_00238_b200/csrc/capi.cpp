@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -377,6 +379,23 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       res->evaluated += b.evaluated;
     }
     res->flops = fl;
+    if (std::getenv("TF_PHASE_DUMP")) {  // tuning aid (TF_PHASE_TIMING builds)
+      double c[4] = {0, 0, 0, 0};
+      for (const BlockStat& b : st)
+        for (int q = 0; q < 4; ++q) c[q] += b.cyc[q];
+      const double n = st.empty() ? 1.0 : static_cast<double>(st.size());
+      std::fprintf(stderr, "phase cycles/block: stage %.0f dft %.0f loop %.0f eval %.0f (%zu blocks)\n",
+                   c[0] / n, c[1] / n, c[2] / n, c[3] / n, st.size());
+      double ic[6] = {0, 0, 0, 0, 0, 0}, its = 0;
+      for (const BlockStat& b : st) {
+        for (int q = 0; q < 6; ++q) ic[q] += b.icyc[q];
+        its += b.iters;
+      }
+      its = its > 0 ? its : 1;
+      std::fprintf(stderr, "per-iteration cycles (thread 0): argmax %.0f reduce+coeff %.0f barrier %.0f "
+                   "decode %.0f bookkeeping %.0f update %.0f\n", ic[0] / its, ic[1] / its, ic[2] / its,
+                   ic[3] / its, ic[4] / its, ic[5] / its);
+    }
   }
   return TF_OK;
 }

@@ -29,6 +29,9 @@ struct BlockStat {
   int32_t pairs;     // non-self-conjugate selections P_b
   int32_t touched;   // touched bins T_b
   int32_t evaluated; // unknown core pixels evaluated (U_b restricted to the core)
+  int32_t cyc[4];    // TF_PHASE_TIMING builds: clock cycles of staging, DFT, loop, evaluate
+  int32_t icyc[6];   // TF_PHASE_TIMING builds, thread 0, summed over iterations: argmax,
+                     // warp-reduce+coeff+slot, barrier, slot-read+decode, bookkeeping, update
 };
 
 struct FseLaunch {
@@ -96,6 +99,8 @@ int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                        cudaStream_t s);
+cudaError_t div_selftest_launch(long long n, unsigned long long seed, unsigned long long* bad,
+                                cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,

@@ -113,3 +113,11 @@ def test_fast_mode_within_tolerance(ctx, fctx):
         assert (d <= 1).mean() >= FAST_WITHIN1
         assert abs(O.psnr(img, ex) - O.psnr(img, fa)) <= FAST_DPSNR_DB
         assert np.array_equal(ex[~unk], img[~unk])
+
+
+def test_hoisted_reciprocal_division_is_exact():
+    import ctypes as C
+    from paper_2207_00238_b200 import _native as N
+    bad = C.c_int64(-1)
+    N.check(N.lib().tf_selftest_div(0, 1 << 24, 12345, C.byref(bad)))
+    assert bad.value == 0
