@@ -121,6 +121,9 @@ struct Gpu {
   int tw_wmax = 0;
   int occ[2][tfb::kNumCfgs] = {};
   int occ_smem[2][tfb::kNumCfgs] = {};
+  int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
+  int wocc_smem[2][33] = {};
+  DevBuf wblocks, wlog_kl, wlog_c;
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
   // ring of (start, stop) events around the most recent FSE kernel launches
   static constexpr int kRing = 256;
@@ -281,6 +284,25 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     g.occ[exact][cfg] = occ;
     g.occ_smem[exact][cfg] = lay.total;
   }
+  // warp-per-block kernel for full windows with 32 % M == 0 (TF_NO_WARP=1 disables)
+  const int span = p.block + 2 * p.margin;
+  int wbpt = (std::getenv("TF_NO_WARP") || span > pl.wmax) ? 0 : tfb::pick_warp_bpt(span, span);
+  // measured: in EXACT mode the 32-bins-per-lane variant is register-bound and slower than
+  // the CTA kernel (c2); 8/16 bins per lane win (c3).  TF_FORCE_WARP=1 overrides.
+  if (exact && wbpt > 16 && !std::getenv("TF_FORCE_WARP")) wbpt = 0;
+  const tfb::WarpLayout wlay(32 * std::max(wbpt, 1), pl.wmax, p.iters);
+  if (wbpt && (!wlay.fits(32 * wbpt, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = 0;
+  if (wbpt && g.wocc_smem[exact][wbpt] != wlay.total) {
+    int occ = 0;
+    TF_CUDA(tfb::fse_warp_prepare(wbpt, exact, wlay.total, &occ));
+    g.wocc[exact][wbpt] = occ;
+    g.wocc_smem[exact][wbpt] = wlay.total;
+  }
+  if (wbpt && g.wocc[exact][wbpt] < 1) wbpt = 0;
+  if (std::getenv("TF_VERBOSE"))
+    std::fprintf(stderr, "[tframe] cta cfg %dx%d smem %d occ %d | warp bpt %d smem %d occ %d\n",
+                 nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wbpt, wlay.total,
+                 wbpt ? g.wocc[exact][wbpt] : 0);
   int rc = upload_tables(g, p, pl.wmax, s);
   if (rc != TF_OK) return rc;
 
@@ -292,6 +314,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   std::memcpy(g.pinned, pl.tiles.data(), n_tiles * sizeof(TileDesc));
   TF_CUDA(g.tiles.ensure(n_tiles * sizeof(TileDesc)));
   TF_CUDA(g.blocks.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+  TF_CUDA(g.wblocks.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
   TF_CUDA(g.counters.ensure(4 * sizeof(int32_t)));
   TF_CUDA(g.refblk.ensure(n_tiles * sizeof(unsigned long long)));
   TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
@@ -299,8 +322,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   TF_CUDA(cudaMemsetAsync(g.counters.p, 0, 4 * sizeof(int32_t), s));
   TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, n_tiles * sizeof(unsigned long long), s));
   if (want_stats) {
-    TF_CUDA(g.stats.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
-    TF_CUDA(cudaMemsetAsync(g.stats.p, 0, static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
+    // [CTA-kernel blocks | warp-kernel blocks]
+    TF_CUDA(g.stats.ensure(2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
+    TF_CUDA(cudaMemsetAsync(g.stats.p, 0, 2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
   }
   const size_t frame_bytes = static_cast<size_t>(W) * H * frames;
   if (d_out != d_img)
@@ -318,6 +342,11 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   e.blocks = g.blocks.as<BlockDesc>();
   e.n_blocks = g.counters.as<int32_t>();
   e.ref_blocks = g.refblk.as<unsigned long long>();
+  e.margin = p.margin;
+  e.warp_M = wbpt ? span : 0;
+  e.warp_L = wbpt ? span : 0;
+  e.wblocks = g.wblocks.as<BlockDesc>();
+  e.n_wblocks = g.counters.as<int32_t>() + 2;
   TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
 
   tfb::FseLaunch a{};
@@ -347,6 +376,19 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   }
   TF_CUDA(cudaEventRecord(g.ev0, s));
   TF_CUDA(cudaEventRecord(g.ring0[slot], s));
+  if (wbpt) {
+    const int wgrid = g.sms * g.wocc[exact][wbpt];
+    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(int32_t)));
+    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(double2)));
+    tfb::FseLaunch w = a;
+    w.blocks = g.wblocks.as<BlockDesc>();
+    w.n_blocks = g.counters.as<int32_t>() + 2;
+    w.next_block = g.counters.as<int32_t>() + 3;
+    w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
+    w.wlog_kl = g.wlog_kl.as<int32_t>();
+    w.wlog_c = g.wlog_c.as<double2>();
+    TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wgrid, wlay.total, s));
+  }
   TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
   TF_CUDA(cudaEventRecord(g.ring1[slot], s));
   TF_CUDA(cudaEventRecord(g.ev1, s));
@@ -365,10 +407,14 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     res->ref_blocks = 0;
     for (size_t t = 0; t < n_tiles; ++t)
       if (static_cast<int>(t % n_parts) == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
-    res->processed = cnt[0];
-    std::vector<BlockStat> st(static_cast<size_t>(cnt[0]));
+    res->processed = cnt[0] + cnt[2];
+    std::vector<BlockStat> st(static_cast<size_t>(cnt[0] + cnt[2]));
     if (cnt[0] > 0)
-      TF_CUDA(cudaMemcpy(st.data(), g.stats.p, st.size() * sizeof(BlockStat), cudaMemcpyDeviceToHost));
+      TF_CUDA(cudaMemcpy(st.data(), g.stats.p, static_cast<size_t>(cnt[0]) * sizeof(BlockStat),
+                         cudaMemcpyDeviceToHost));
+    if (cnt[2] > 0)
+      TF_CUDA(cudaMemcpy(st.data() + cnt[0], g.stats.as<BlockStat>() + pl.cand_blocks,
+                         static_cast<size_t>(cnt[2]) * sizeof(BlockStat), cudaMemcpyDeviceToHost));
     // F_b = 2(4NM + 8NL) + 3N I_b + 8N (I_b + P_b) + 14 U_b T_b
     double fl = 0.0;
     for (const BlockStat& b : st) {
@@ -484,7 +530,8 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.stream) cudaStreamSynchronize(g.stream);
     if (g.comm && nccl().ok) nccl().CommDestroy(g.comm);
     for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
-                      &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv})
+                      &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv, &g.wblocks,
+                      &g.wlog_kl, &g.wlog_c})
       b->release();
     if (g.pinned) cudaFreeHost(g.pinned);
     for (int r = 0; r < Gpu::kRing; ++r) {
@@ -654,7 +701,7 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       kms = std::max(kms, static_cast<double>(ms));
       int32_t cnt[4];
       TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
-      stats->blocks_processed += cnt[0];
+      stats->blocks_processed += cnt[0] + cnt[2];
       std::vector<unsigned long long> ref(pl.tiles.size());
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));

@@ -49,6 +49,8 @@ struct FseLaunch {
   const double* tw;       // twiddles (cos,sin) interleaved, sizes n=1..wmax at n*(n-1)/2
   int32_t wmax;           // max window side in this launch
   BlockStat* stats;       // optional
+  int32_t* wlog_kl;       // warp kernel: per-CTA selection log scratch (iters entries each)
+  double2* wlog_c;
 };
 
 struct EnumLaunch {
@@ -57,35 +59,57 @@ struct EnumLaunch {
   const TileDesc* tiles;
   int32_t n_tiles;
   int32_t part, n_parts;      // only tiles t % n_parts == part are enqueued
-  BlockDesc* blocks;          // out
-  int32_t* n_blocks;          // out: processed-block count
+  BlockDesc* blocks;          // out: blocks for the CTA kernel
+  int32_t* n_blocks;          // out: their count
   unsigned long long* ref_blocks;  // out, per tile: blocks the reference processes
+  int32_t margin;
+  int32_t warp_M, warp_L;     // windows of exactly this size go to the warp kernel (0 = none)
+  BlockDesc* wblocks;         // out: blocks for the warp kernel
+  int32_t* n_wblocks;
 };
 
 constexpr int kCY = 4;  // rows per DFT chunk
 
 // Shared-memory layout of the FSE kernel (bytes), computed identically on host and device.
-//   [W replicated along k: double2 x L x 2M <= 2*nb][twiddles: double2 x 2*wmax][union][slots][misc]
-//   union = DFT phase {cw, cwv: double x kCY*wmax; rw, rr: double2 x kCY*wmax; pix, kn: u8 x nb}
-//         | loop phase {mval: double2 x cap; lst: int32 x cap; pos: int16 x nb}
+//   [W replicated (2L x M or L x 2M double2, <= 2*nb)][twiddles: double2 x 2*wmax][union][slots][misc]
+//   union = DFT phase {cwp, rw, rr: double2 x kCY*wmax; pix, kn: u8 x nb}
+//         | loop phase {selection log: double2 x iters, int32 x iters}
+//   after the loop the W region holds the model {mval: double2 x cap; lst: int32 x cap;
+//   pos: int16 x nb} (cap = min(2I, nb) distinct touched bins).
 struct SmemLayout {
   int nb, wmax, iters, nw, cap;
-  int off_tw, off_union, off_pix, off_kn, off_lst, off_pos, off_slots, off_misc, total;
+  int off_tw, off_union, off_pix, off_kn, off_lst, off_slots, off_misc, total;
   __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
   __host__ __device__ SmemLayout(int nb_, int wmax_, int iters_, int nw_)
       : nb(nb_), wmax(wmax_), iters(iters_), nw(nw_) {
-    cap = iters >= (nb + 1) / 2 ? nb : 2 * iters;  // touched bins are distinct: <= min(2I, N)
+    cap = iters >= (nb + 1) / 2 ? nb : 2 * iters;
     off_tw = 32 * nb;
     off_union = off_tw + align16(2 * 16 * wmax);
     off_pix = off_union + 48 * kCY * wmax;
     off_kn = off_pix + nb;
     const int dft_end = off_kn + nb;
-    off_lst = off_union + 16 * cap;
-    off_pos = off_lst + 4 * cap;
-    const int loop_end = off_pos + 2 * nb;
+    off_lst = off_union + 16 * iters;  // int32 log after the double2 log
+    const int loop_end = off_lst + 4 * iters;
     off_slots = align16(dft_end > loop_end ? dft_end : loop_end);
     off_misc = off_slots + 2 * nw * 32;
     total = off_misc + 16;
+  }
+};
+
+// Warp-per-block kernel layout: [W replicated 2L x M: 32*N B][twiddles 32*wmax B][misc 16 B];
+// the DFT scratch lives in W's second copy until the copy is written.
+struct WarpLayout {
+  int n, wmax, cap, off_tw, off_misc, off_log, total;
+  __host__ __device__ WarpLayout(int n_, int wmax_, int iters) : n(n_), wmax(wmax_) {
+    cap = iters >= (n + 1) / 2 ? n : 2 * iters;
+    off_tw = 32 * n;
+    off_misc = off_tw + 32 * wmax;
+    total = off_misc + 16;
+    off_log = (20 * cap + 2 * n + 15) & ~15;  // post-loop copy of the log inside W's space
+  }
+  __host__ __device__ bool fits(int n_, int wmax_, int iters) const {
+    // DFT scratch in the second copy; post-loop model + log copy inside W's space
+    return 48 * kCY * wmax_ + 2 * n_ <= 16 * n_ && off_log + 20 * iters <= 32 * n_;
   }
 };
 
@@ -101,6 +125,11 @@ cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int sm
                        cudaStream_t s);
 cudaError_t div_selftest_launch(long long n, unsigned long long seed, unsigned long long* bad,
                                 cudaStream_t s);
+// warp kernel variants: bins per lane (window M*L = 32*bpt with 32 % M == 0)
+int pick_warp_bpt(int M, int L);  // 0 if no variant
+cudaError_t fse_warp_prepare(int bpt, bool exact, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_warp_launch(int bpt, bool exact, const FseLaunch& a, int grid, int smem_bytes,
+                            cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,
