@@ -1,0 +1,130 @@
+// tframe_b200.hpp — header-only C++ mirror of the reference's extrapolator and
+// tiling interface (tframe, extrapolate.hpp:22-36, runtime.hpp:35-139) on top of
+// the C-ABI in tframe_fse.h.  It does not depend on the reference headers; see
+// INTEGRATION.md for the 20-line adapter that derives tframe::Extrapolator from it.
+//
+// Error behaviour mirrors the reference: invalid parameters / dimensions throw
+// std::invalid_argument, degenerate tilings throw tfb200::TilingError, anything
+// else (CUDA, NCCL) throws tfb200::Error.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tframe_fse.h"
+
+namespace tfb200 {
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct TilingError : Error {
+  using Error::Error;
+};
+
+inline void check(int rc) {
+  if (rc == TF_OK) return;
+  const std::string msg = tf_last_error(nullptr);
+  if (rc == TF_EINVAL) throw std::invalid_argument(msg);
+  if (rc == TF_ETILING) throw TilingError(msg);
+  throw Error("[tf status " + std::to_string(rc) + "] " + msg);
+}
+
+// extrapolate.hpp:86-92
+struct FseLiteParams {
+  int block_size = 4;
+  int support_margin = 8;
+  int model_iterations = 100;
+  double compensation = 0.5;  // gamma
+  double weight_decay = 0.8;  // rho
+  tf_fse_params c() const {
+    return tf_fse_params{block_size, support_margin, model_iterations, compensation, weight_decay};
+  }
+};
+
+// Owns per-GPU streams, device buffers and NCCL communicators (tf_ctx).
+class Context {
+ public:
+  explicit Context(int n_gpus = 1, const std::vector<int>& devices = {}, int mode = TF_MODE_EXACT)
+      : h_(tf_create(n_gpus, devices.empty() ? nullptr : devices.data()), &tf_destroy) {
+    if (!h_) throw Error(tf_last_error(nullptr));
+    check(tf_set_mode(h_.get(), mode));
+  }
+  tf_ctx* get() const { return h_.get(); }
+
+ private:
+  std::unique_ptr<tf_ctx, void (*)(tf_ctx*)> h_;
+};
+
+// FseLiteExtrapolator (extrapolate.hpp:390-414) computed on B200s.  Images are
+// row-major u8 (stride = width); masks u8, nonzero = known.
+class FseLiteExtrapolator {
+ public:
+  explicit FseLiteExtrapolator(FseLiteParams p = {}, std::shared_ptr<Context> ctx = nullptr)
+      : p_(p), ctx_(ctx ? std::move(ctx) : std::make_shared<Context>()) {
+    const tf_fse_params c = p_.c();
+    check(tf_check_fse_params(&c));
+  }
+  std::string name() const { return "fse-lite"; }
+  int influence_radius() const { return p_.block_size + p_.support_margin; }
+  std::string params_string() const {
+    char buf[256];
+    const tf_fse_params c = p_.c();
+    check(tf_fse_params_to_string(&c, buf, sizeof buf));
+    return buf;
+  }
+  const FseLiteParams& params() const { return p_; }
+  std::vector<uint8_t> extrapolate(const std::vector<uint8_t>& image, const std::vector<uint8_t>& known,
+                                   int width, int height) const {
+    if (image.size() != known.size() || image.size() != static_cast<size_t>(width) * height)
+      throw std::invalid_argument("fse_lite_extrapolate: image/mask dimension mismatch");
+    std::vector<uint8_t> out(image.size());
+    const tf_fse_params c = p_.c();
+    check(tf_fse_extrapolate(ctx_->get(), image.data(), known.data(), width, height, &c, out.data()));
+    return out;
+  }
+
+ private:
+  FseLiteParams p_;
+  std::shared_ptr<Context> ctx_;
+};
+
+// registry_lookup("fse-lite", "key=value,...") (extrapolate.hpp:418-437)
+inline FseLiteExtrapolator registry_lookup(const std::string& name, const std::string& params = "",
+                                           std::shared_ptr<Context> ctx = nullptr) {
+  if (name != "fse-lite")
+    throw std::invalid_argument("unknown algorithm '" + name + "', available: diffusion, fse-lite");
+  tf_fse_params c{};
+  check(tf_fse_params_from_string(params.c_str(), &c));
+  return FseLiteExtrapolator(FseLiteParams{c.block, c.margin, c.iters, c.gamma, c.rho}, std::move(ctx));
+}
+
+// run_master (runtime.hpp:75-139): plan -> expand -> FSE per halo -> crop -> merge on the
+// context's GPUs; frames stacked.  Returns the merged frames and fills stats.
+inline std::vector<uint8_t> run_master(Context& ctx, const std::vector<uint8_t>& image,
+                                       const std::vector<uint8_t>& known, int W, int H, int frames,
+                                       int tiles, int overlap, const FseLiteParams& p,
+                                       tf_run_stats* stats = nullptr) {
+  std::vector<uint8_t> out(image.size());
+  const tf_fse_params c = p.c();
+  check(tf_tiled_extrapolate(ctx.get(), image.data(), known.data(), W, H, frames, tiles, overlap, &c,
+                             out.data(), stats));
+  return out;
+}
+
+// plan_proposed (tiling.hpp:99-111) + expand (overlap.hpp:25-34)
+inline std::vector<tf_rect> plan_proposed(int W, int H, int N) {
+  std::vector<tf_rect> t(static_cast<size_t>(N > 0 ? N : 0));
+  check(tf_plan_proposed(W, H, N, t.data()));
+  return t;
+}
+inline tf_rect expand(const tf_rect& core, int d, int W, int H) {
+  tf_rect h{};
+  check(tf_expand(&core, d, W, H, &h));
+  return h;
+}
+
+}  // namespace tfb200

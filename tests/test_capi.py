@@ -78,3 +78,20 @@ def test_configs_table():
     assert CONFIGS[2].tiles == 4 and CONFIGS[2].overlap == 12
     assert CONFIGS[2].params.support_margin == 12 and CONFIGS[2].params.model_iterations == 200
     assert CONFIGS[5].frames == 64
+
+
+def test_cpp_adapter_header_compiles_and_runs(tmp_path):
+    """include/tframe_b200.hpp (the C++ mirror of the reference interface) builds against the
+    library and behaves like the reference on host-only calls."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    root = N.LIB_PATH.parent.parent.parent
+    exe = tmp_path / "adapter_smoke"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", str(root / "include"),
+                    str(root / "tests" / "cpp" / "adapter_smoke.cpp"), "-o", str(exe),
+                    "-L", str(N.LIB_PATH.parent), "-ltframe_b200",
+                    f"-Wl,-rpath,{N.LIB_PATH.parent}"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
