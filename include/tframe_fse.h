@@ -91,6 +91,8 @@ typedef struct tf_run_stats {
   double flops;            /* sum of F_b over processed blocks  */
   int64_t iterations;      /* sum of executed iterations I_b                  */
   int64_t pixels_evaluated;/* unknown core pixels written by the model        */
+  double flops_executed;   /* FP64 flops the kernels actually execute (differs
+                              from `flops` for the FAST half-spectrum kernel)  */
 } tf_run_stats;
 
 typedef struct tf_ctx tf_ctx;

@@ -33,7 +33,8 @@ class tf_run_stats(C.Structure):
                 ("total_us", C.c_int64), ("overhead_pixels", C.c_int64),
                 ("blocks_reference", C.c_int64), ("blocks_processed", C.c_int64),
                 ("kernel_ms", C.c_double), ("flops", C.c_double),
-                ("iterations", C.c_int64), ("pixels_evaluated", C.c_int64)]
+                ("iterations", C.c_int64), ("pixels_evaluated", C.c_int64),
+                ("flops_executed", C.c_double)]
 
 
 _u8p = C.POINTER(C.c_uint8)

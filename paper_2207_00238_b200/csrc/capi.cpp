@@ -111,6 +111,8 @@ struct Gpu {
   int dev = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;      // border-window CTA kernel, concurrent with the warp kernel
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_tables = nullptr;
   DevBuf img, known, out;                       // host-API frame buffers
   DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv;
@@ -259,7 +261,7 @@ static int make_plan(int W, int H, int frames, int n_tiles, int overlap, int B, 
 
 struct DevRun {
   int64_t ref_blocks = 0, processed = 0, iterations = 0, evaluated = 0;
-  double kernel_ms = 0.0, flops = 0.0;
+  double kernel_ms = 0.0, flops = 0.0, flops_executed = 0.0;
 };
 
 // Enqueue one GPU's share (tiles t % n_parts == part) of a tiled job.
@@ -284,24 +286,41 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     g.occ[exact][cfg] = occ;
     g.occ_smem[exact][cfg] = lay.total;
   }
-  // warp-per-block kernel for full windows with 32 % M == 0 (TF_NO_WARP=1 disables)
+  // warp-per-block kernels for full windows (TF_NO_WARP=1 disables):
+  //  EXACT: fse_warp_kernel when 32 % span == 0 and 8 or 16 bins per lane (measured: the
+  //         32-bins-per-lane variant is register-bound and slower than the CTA kernel);
+  //  FAST:  fse_warp_half_kernel (Hermitian half spectrum) for span in {8, 16, 32}.
   const int span = p.block + 2 * p.margin;
-  int wbpt = (std::getenv("TF_NO_WARP") || span > pl.wmax) ? 0 : tfb::pick_warp_bpt(span, span);
-  // measured: in EXACT mode the 32-bins-per-lane variant is register-bound and slower than
-  // the CTA kernel (c2); 8/16 bins per lane win (c3).  TF_FORCE_WARP=1 overrides.
-  if (exact && wbpt > 16 && !std::getenv("TF_FORCE_WARP")) wbpt = 0;
-  const tfb::WarpLayout wlay(32 * std::max(wbpt, 1), pl.wmax, p.iters);
-  if (wbpt && (!wlay.fits(32 * wbpt, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = 0;
-  if (wbpt && g.wocc_smem[exact][wbpt] != wlay.total) {
-    int occ = 0;
-    TF_CUDA(tfb::fse_warp_prepare(wbpt, exact, wlay.total, &occ));
-    g.wocc[exact][wbpt] = occ;
-    g.wocc_smem[exact][wbpt] = wlay.total;
+  const bool nowarp = std::getenv("TF_NO_WARP") || span > pl.wmax;
+  int wbpt = 0, wkind = 0;  // 1 = exact warp kernel, 2 = FAST half-spectrum warp kernel
+  if (!nowarp && exact) {
+    wbpt = tfb::pick_warp_bpt(span, span);
+    if (wbpt > 16 && !std::getenv("TF_FORCE_WARP")) wbpt = 0;
+    wkind = wbpt ? 1 : 0;
+  } else if (!nowarp) {
+    wbpt = tfb::pick_warp_half_bpth(span, span);
+    wkind = wbpt ? 2 : 0;
   }
-  if (wbpt && g.wocc[exact][wbpt] < 1) wbpt = 0;
+  const int wn = span * span;
+  const tfb::WarpLayout wlay(std::max(wn, 32), pl.wmax, p.iters);
+  if (wbpt && (!wlay.fits(wn, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = wkind = 0;
+  // FAST half kernel: W rows + partial copy, log (20 B/iteration) reuses W's space after the loop
+  const tfb::HalfLayout hlay(span, span, std::max(wbpt, 1), pl.wmax);
+  if (wkind == 2 && (20 * p.iters > hlay.wbytes || hlay.total > 227 * 1024)) wbpt = wkind = 0;
+  const int wsmem = wkind == 2 ? hlay.total : wlay.total;
+  if (wbpt && g.wocc_smem[exact][wbpt] != wsmem) {
+    int occ = 0;
+    if (wkind == 1)
+      TF_CUDA(tfb::fse_warp_prepare(wbpt, exact, wsmem, &occ));
+    else
+      TF_CUDA(tfb::fse_warp_half_prepare(wbpt, wsmem, &occ));
+    g.wocc[exact][wbpt] = occ;
+    g.wocc_smem[exact][wbpt] = wsmem;
+  }
+  if (wbpt && g.wocc[exact][wbpt] < 1) wbpt = wkind = 0;
   if (std::getenv("TF_VERBOSE"))
-    std::fprintf(stderr, "[tframe] cta cfg %dx%d smem %d occ %d | warp bpt %d smem %d occ %d\n",
-                 nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wbpt, wlay.total,
+    std::fprintf(stderr, "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d\n",
+                 nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
                  wbpt ? g.wocc[exact][wbpt] : 0);
   int rc = upload_tables(g, p, pl.wmax, s);
   if (rc != TF_OK) return rc;
@@ -376,7 +395,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   }
   TF_CUDA(cudaEventRecord(g.ev0, s));
   TF_CUDA(cudaEventRecord(g.ring0[slot], s));
+  const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
   if (wbpt) {
+    // border windows (CTA kernel) on a forked stream, concurrently with the warp kernel
+    TF_CUDA(cudaEventRecord(g.ev_fork, s));
+    TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
+    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
+    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
     const int wgrid = g.sms * g.wocc[exact][wbpt];
     TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(int32_t)));
     TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(double2)));
@@ -387,9 +412,20 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
     w.wlog_kl = g.wlog_kl.as<int32_t>();
     w.wlog_c = g.wlog_c.as<double2>();
-    TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wgrid, wlay.total, s));
+    if (wkind == 1)
+      TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wgrid, wsmem, s));
+    else
+      TF_CUDA(tfb::fse_warp_half_launch(wbpt, w, wgrid, wsmem, s));
+    TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
+  } else {
+    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
   }
-  TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
+  if (ktime) {
+    TF_CUDA(cudaStreamSynchronize(s));
+    int32_t cnt[4];
+    TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[tframe] warp blocks %d, cta blocks %d\n", cnt[2], cnt[0]);
+  }
   TF_CUDA(cudaEventRecord(g.ring1[slot], s));
   TF_CUDA(cudaEventRecord(g.ev1, s));
   ++g.launches;
@@ -415,16 +451,30 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     if (cnt[2] > 0)
       TF_CUDA(cudaMemcpy(st.data() + cnt[0], g.stats.as<BlockStat>() + pl.cand_blocks,
                          static_cast<size_t>(cnt[2]) * sizeof(BlockStat), cudaMemcpyDeviceToHost));
-    // F_b = 2(4NM + 8NL) + 3N I_b + 8N (I_b + P_b) + 14 U_b T_b
-    double fl = 0.0;
-    for (const BlockStat& b : st) {
+    // algorithmic F_b = 2(4NM + 8NL) + 3N I_b + 8N (I_b + P_b) + 14 U_b T_b;
+    // executed flops differ only for the FAST half-spectrum warp kernel (wkind 2), which
+    // runs the row pass fully, the column pass / update / argmax on rows l <= L/2 only and
+    // evaluates from the log: 8 M^2 L + 16 Nh L + Nh (11 I_b + 8 P_b) + 11 U_b I_b,
+    // Nh = rows carried * M (T_b there is reported as I_b + P_b, an upper bound).
+    double fl = 0.0, xfl = 0.0;
+    for (size_t q = 0; q < st.size(); ++q) {
+      const BlockStat& b = st[q];
       const double N = static_cast<double>(b.M) * b.L;
-      fl += 2.0 * (4.0 * N * b.M + 8.0 * N * b.L) + 3.0 * N * b.iters +
-            8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
+      const double f = 2.0 * (4.0 * N * b.M + 8.0 * N * b.L) + 3.0 * N * b.iters +
+                       8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
+      fl += f;
+      if (wkind == 2 && q >= static_cast<size_t>(cnt[0])) {
+        const double Nh = static_cast<double>(wbpt) * 32.0;
+        xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
+               11.0 * b.evaluated * b.iters;
+      } else {
+        xfl += f;
+      }
       res->iterations += b.iters;
       res->evaluated += b.evaluated;
     }
     res->flops = fl;
+    res->flops_executed = xfl;
     if (std::getenv("TF_PHASE_DUMP")) {  // tuning aid (TF_PHASE_TIMING builds)
       double c[4] = {0, 0, 0, 0};
       for (const BlockStat& b : st)
@@ -514,6 +564,9 @@ tf_ctx* tf_create(int n_gpus, const int* device_ids) {
     g.sms = prop.multiProcessorCount;
     if (cudaSetDevice(g.dev) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&g.ev0) != cudaSuccess || cudaEventCreate(&g.ev1) != cudaSuccess ||
         cudaEventCreateWithFlags(&g.ev_tables, cudaEventDisableTiming) != cudaSuccess) {
       set_error(TF_ECUDA, "tf_create: stream/event creation failed");
@@ -541,6 +594,10 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.ev0) cudaEventDestroy(g.ev0);
     if (g.ev1) cudaEventDestroy(g.ev1);
     if (g.ev_tables) cudaEventDestroy(g.ev_tables);
+    if (g.side) cudaStreamSynchronize(g.side);
+    if (g.ev_fork) cudaEventDestroy(g.ev_fork);
+    if (g.ev_join) cudaEventDestroy(g.ev_join);
+    if (g.side) cudaStreamDestroy(g.side);
     if (g.stream) cudaStreamDestroy(g.stream);
   }
   if (ctx->rank_comm && nccl().ok) nccl().CommDestroy(ctx->rank_comm);
@@ -588,6 +645,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
     stats->blocks_processed = dr.processed;
     stats->kernel_ms = dr.kernel_ms;
     stats->flops = dr.flops;
+    stats->flops_executed = dr.flops_executed;
     stats->iterations = dr.iterations;
     stats->pixels_evaluated = dr.evaluated;
   }

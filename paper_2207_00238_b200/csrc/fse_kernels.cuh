@@ -113,6 +113,22 @@ struct WarpLayout {
   }
 };
 
+// FAST half-spectrum warp kernel layout: W rows 0..L-1 plus a copy of rows 0..lmax
+// (the gathers touch rows 1..L+lmax only), the DFT scratch above row L until that copy
+// is written; then the twiddles and misc.  lmax = bpth * (32 / M) - 1.
+struct HalfLayout {
+  int wbytes, off_tw, total;
+  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax) {
+    const int lmax = bpth * (32 / M) - 1;
+    const int rows = 16 * M * (L + lmax + 1);
+    const int scratch = 16 * M * L + 48 * kCY * wmax + 2 * M * L;
+    wbytes = (rows > scratch ? rows : scratch);
+    wbytes = (wbytes + 15) & ~15;
+    off_tw = wbytes;
+    total = off_tw + 32 * wmax + 16;
+  }
+};
+
 // ---- launch helpers (fse_kernels.cu)
 struct KernelCfg {
   int nt, bpt;
@@ -130,6 +146,11 @@ int pick_warp_bpt(int M, int L);  // 0 if no variant
 cudaError_t fse_warp_prepare(int bpt, bool exact, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_warp_launch(int bpt, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                             cudaStream_t s);
+// FAST-mode Hermitian half-spectrum warp kernel (window M = L in {8, 16, 32})
+int pick_warp_half_bpth(int M, int L);  // 0 if no variant
+cudaError_t fse_warp_half_prepare(int bpth, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_warp_half_launch(int bpth, const FseLaunch& a, int grid, int smem_bytes,
+                                 cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,

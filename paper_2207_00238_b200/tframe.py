@@ -314,13 +314,14 @@ class RunStats:
     flops: float = 0.0
     iterations: int = 0
     pixels_evaluated: int = 0
+    flops_executed: float = 0.0
     tiles: list = field(default_factory=list)
 
     @classmethod
     def _from_c(cls, s: N.tf_run_stats) -> "RunStats":
         return cls(s.plan_us, s.distribute_us, s.compute_span_us, s.merge_us, s.total_us,
                    s.overhead_pixels, s.blocks_reference, s.blocks_processed, s.kernel_ms,
-                   s.flops, s.iterations, s.pixels_evaluated)
+                   s.flops, s.iterations, s.pixels_evaluated, s.flops_executed)
 
 
 def run_master(image: np.ndarray, mask: np.ndarray, config: MasterConfig,

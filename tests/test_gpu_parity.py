@@ -121,3 +121,36 @@ def test_hoisted_reciprocal_division_is_exact():
     bad = C.c_int64(-1)
     N.check(N.lib().tf_selftest_div(0, 1 << 24, 12345, C.byref(bad)))
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_fast_mode_full_config_frame_within_tolerance(ctx, fctx, cfg):
+    """FAST mode (FMA, Hermitian half-spectrum warp kernel) on a full BASELINE frame:
+    >= 99.9% of reconstructed pixels within +-1 of EXACT (== reference) and
+    |PSNR(fast) - PSNR(exact)| <= 0.05 dB against the ground truth; argmax divergences
+    show up as the residual disagreements and are reported in the assertion message."""
+    wl = CONFIGS[cfg]
+    img, kn = T.synth_frame(cfg, 0, wl.W, wl.H)
+    ex, st_e = ctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+    fa, st_f = fctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+    unk = kn == 0
+    d = np.abs(ex.astype(int) - fa.astype(int))[unk]
+    within1 = float((d <= 1).mean())
+    dpsnr = abs(O.psnr(img, ex) - O.psnr(img, fa))
+    msg = f"c{cfg}: within1={within1:.5f} max|d|={d.max()} n(|d|>1)={(d > 1).sum()} dPSNR={dpsnr:.4f} dB"
+    assert within1 >= FAST_WITHIN1, msg
+    assert dpsnr <= FAST_DPSNR_DB, msg
+    assert np.array_equal(fa[~unk], img[~unk])
+    assert st_e.blocks_processed == st_f.blocks_processed
+
+
+def test_exact_mode_full_c2_frame_equals_oracle(ctx):
+    """Byte-identical on a full 1920x1080 config-2 frame (4 tiles, d=12) vs the C oracle."""
+    wl = CONFIGS[2]
+    img, kn = T.synth_frame(2, 1, wl.W, wl.H)
+    p = wl.params
+    want, bpt = O.tiled(img, kn, wl.tiles, wl.overlap, p.block_size, p.support_margin,
+                        p.model_iterations, p.compensation, p.weight_decay)
+    got, st = ctx.tiled(img, kn, wl.tiles, wl.overlap, p)
+    assert int((got != want).sum()) == 0
+    assert st.blocks_reference == int(bpt.sum())
