@@ -125,6 +125,8 @@ struct Gpu {
   int occ_smem[2][tfb::kNumCfgs] = {};
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
+  int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
+  int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
   // ring of (start, stop) events around the most recent FSE kernel launches
@@ -289,23 +291,26 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // warp-per-block kernels for full windows (TF_NO_WARP=1 disables):
   //  EXACT: fse_warp_kernel when 32 % span == 0 and 8 or 16 bins per lane (measured: the
   //         32-bins-per-lane variant is register-bound and slower than the CTA kernel);
-  //  FAST:  fse_warp_half_kernel (Hermitian half spectrum) for span in {8, 16, 32}.
+  //  FAST:  fse_half_kernel (Hermitian half spectrum) for span in {8, 16, 32}, one or two
+  //         warps per block (TF_HALF_NT=32|64 overrides the per-span default).
   const int span = p.block + 2 * p.margin;
   const bool nowarp = std::getenv("TF_NO_WARP") || span > pl.wmax;
   int wbpt = 0, wkind = 0;  // 1 = exact warp kernel, 2 = FAST half-spectrum warp kernel
+  int hnt = 32;  // threads per block of the half-spectrum kernel (measured: 64 is slower)
+  if (const char* e = std::getenv("TF_HALF_NT")) hnt = std::atoi(e);
   if (!nowarp && exact) {
     wbpt = tfb::pick_warp_bpt(span, span);
     if (wbpt > 16 && !std::getenv("TF_FORCE_WARP")) wbpt = 0;
     wkind = wbpt ? 1 : 0;
   } else if (!nowarp) {
-    wbpt = tfb::pick_warp_half_bpth(span, span);
+    wbpt = tfb::pick_half_bpth(hnt, span, span);
     wkind = wbpt ? 2 : 0;
   }
   const int wn = span * span;
   const tfb::WarpLayout wlay(std::max(wn, 32), pl.wmax, p.iters);
   if (wbpt && (!wlay.fits(wn, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = wkind = 0;
   // FAST half kernel: W rows + partial copy, log (20 B/iteration) reuses W's space after the loop
-  const tfb::HalfLayout hlay(span, span, std::max(wbpt, 1), pl.wmax);
+  const tfb::HalfLayout hlay(span, span, std::max(wbpt, 1), pl.wmax, hnt);
   if (wkind == 2 && (20 * p.iters > hlay.wbytes || hlay.total > 227 * 1024)) wbpt = wkind = 0;
   const int wsmem = wkind == 2 ? hlay.total : wlay.total;
   if (wbpt && g.wocc_smem[exact][wbpt] != wsmem) {
@@ -313,15 +318,31 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     if (wkind == 1)
       TF_CUDA(tfb::fse_warp_prepare(wbpt, exact, wsmem, &occ));
     else
-      TF_CUDA(tfb::fse_warp_half_prepare(wbpt, wsmem, &occ));
+      TF_CUDA(tfb::fse_half_prepare(hnt, wbpt, wsmem, &occ));
     g.wocc[exact][wbpt] = occ;
     g.wocc_smem[exact][wbpt] = wsmem;
   }
   if (wbpt && g.wocc[exact][wbpt] < 1) wbpt = wkind = 0;
+  // FAST: clamped border windows through the GEN half kernel instead of the CTA kernel
+  int gbpth = 0;
+  if (wkind == 2 && !std::getenv("TF_NO_GEN")) {
+    gbpth = span / 2 + 1;
+    const tfb::HalfLayout glay(32, span, gbpth, std::max(pl.wmax, 32), 32);
+    if (20 * p.iters > glay.wbytes || glay.total > 227 * 1024) gbpth = 0;
+    if (gbpth && g.gocc_smem[gbpth] != glay.total) {
+      int occ = 0;
+      TF_CUDA(tfb::fse_half_prepare(0, gbpth, glay.total, &occ));
+      g.gocc[gbpth] = occ;
+      g.gocc_smem[gbpth] = glay.total;
+    }
+    if (gbpth && g.gocc[gbpth] < 1) gbpth = 0;
+  }
+  const int gsmem = gbpth ? tfb::HalfLayout(32, span, gbpth, std::max(pl.wmax, 32), 32).total : 0;
   if (std::getenv("TF_VERBOSE"))
-    std::fprintf(stderr, "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d\n",
+    std::fprintf(stderr,
+                 "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d\n",
                  nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
-                 wbpt ? g.wocc[exact][wbpt] : 0);
+                 wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0);
   int rc = upload_tables(g, p, pl.wmax, s);
   if (rc != TF_OK) return rc;
 
@@ -400,11 +421,19 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     // border windows (CTA kernel) on a forked stream, concurrently with the warp kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
-    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
-    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
     const int wgrid = g.sms * g.wocc[exact][wbpt];
-    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(int32_t)));
-    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(double2)));
+    const int ggrid = gbpth ? std::min(g.sms * g.gocc[gbpth], std::max(grid, 1)) : 0;
+    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid + ggrid) * p.iters * sizeof(int32_t)));
+    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid + ggrid) * p.iters * sizeof(double2)));
+    if (gbpth) {
+      tfb::FseLaunch ga = a;
+      ga.wlog_kl = g.wlog_kl.as<int32_t>() + static_cast<size_t>(wgrid) * p.iters;
+      ga.wlog_c = g.wlog_c.as<double2>() + static_cast<size_t>(wgrid) * p.iters;
+      TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, g.side));
+    } else {
+      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
+    }
+    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
     tfb::FseLaunch w = a;
     w.blocks = g.wblocks.as<BlockDesc>();
     w.n_blocks = g.counters.as<int32_t>() + 2;
@@ -415,7 +444,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     if (wkind == 1)
       TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wgrid, wsmem, s));
     else
-      TF_CUDA(tfb::fse_warp_half_launch(wbpt, w, wgrid, wsmem, s));
+      TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wgrid, wsmem, s));
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));

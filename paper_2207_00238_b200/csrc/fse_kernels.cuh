@@ -117,15 +117,16 @@ struct WarpLayout {
 // (the gathers touch rows 1..L+lmax only), the DFT scratch above row L until that copy
 // is written; then the twiddles and misc.  lmax = bpth * (32 / M) - 1.
 struct HalfLayout {
-  int wbytes, off_tw, total;
-  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax) {
-    const int lmax = bpth * (32 / M) - 1;
+  int wbytes, off_tw, off_sync, total;
+  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt) {
+    const int lmax = bpth * (nt / M) - 1;
     const int rows = 16 * M * (L + lmax + 1);
     const int scratch = 16 * M * L + 48 * kCY * wmax + 2 * M * L;
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
-    total = off_tw + 32 * wmax + 16;
+    off_sync = off_tw + 32 * wmax;
+    total = off_sync + (nt == 64 ? 4 * 32 + 16 : 16);  // argmax slots + block id (two warps)
   }
 };
 
@@ -147,9 +148,9 @@ cudaError_t fse_warp_prepare(int bpt, bool exact, int smem_bytes, int* ctas_per_
 cudaError_t fse_warp_launch(int bpt, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                             cudaStream_t s);
 // FAST-mode Hermitian half-spectrum warp kernel (window M = L in {8, 16, 32})
-int pick_warp_half_bpth(int M, int L);  // 0 if no variant
-cudaError_t fse_warp_half_prepare(int bpth, int smem_bytes, int* ctas_per_sm);
-cudaError_t fse_warp_half_launch(int bpth, const FseLaunch& a, int grid, int smem_bytes,
+int pick_half_bpth(int nt, int M, int L);  // 0 if no variant
+cudaError_t fse_half_prepare(int nt, int bpth, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_half_launch(int nt, int bpth, const FseLaunch& a, int grid, int smem_bytes,
                                  cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,

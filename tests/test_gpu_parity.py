@@ -115,6 +115,25 @@ def test_fast_mode_within_tolerance(ctx, fctx):
         assert np.array_equal(ex[~unk], img[~unk])
 
 
+def test_fast_mode_border_windows(ctx, fctx):
+    """Small, odd-sized frames: most windows are clamped by the halo (M, L not powers of two),
+    which the FAST path runs through the GEN half-spectrum kernel."""
+    ds, n = [], 0
+    for cfg in (2, 3):
+        wl = CONFIGS[cfg]
+        for (W, H), tiles in (((37, 29), 1), ((61, 44), 2), ((100, 57), 3), ((45, 90), 4)):
+            img, kn = T.synth_frame(cfg, 3, W, H)
+            ex, st_e = ctx.tiled(img, kn, tiles, wl.overlap, wl.params)
+            fa, st_f = fctx.tiled(img, kn, tiles, wl.overlap, wl.params)
+            unk = kn == 0
+            ds.append(np.abs(ex.astype(int) - fa.astype(int))[unk])
+            assert np.array_equal(fa[~unk], img[~unk])
+            assert st_e.blocks_processed == st_f.blocks_processed
+    d = np.concatenate(ds)
+    assert d.size > 1000
+    assert (d <= 1).mean() >= FAST_WITHIN1, f"max|d|={d.max()} n(|d|>1)={(d > 1).sum()} of {d.size}"
+
+
 def test_hoisted_reciprocal_division_is_exact():
     import ctypes as C
     from paper_2207_00238_b200 import _native as N
