@@ -116,17 +116,22 @@ struct WarpLayout {
 // FAST half-spectrum warp kernel layout: W rows 0..L-1 plus a copy of rows 0..lmax
 // (the gathers touch rows 1..L+lmax only), the DFT scratch above row L until that copy
 // is written; then the twiddles and misc.  lmax = bpth * (32 / M) - 1.
+#ifndef TF_HALF_W32
+#define TF_HALF_W32 0  // 1: half kernels keep W as FP32 complex (8 B); 2: also the correction in FP32
+#endif
+constexpr int kHalfWB = TF_HALF_W32 ? 8 : 16;  // bytes per W element in the half kernels
+
 struct HalfLayout {
   int wbytes, off_tw, off_sync, total;
   __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt) {
     const int lmax = bpth * (nt / M) - 1;
-    const int rows = 16 * M * (L + lmax + 1);
-    const int scratch = 16 * M * L + 48 * kCY * wmax + 2 * M * L;
+    const int rows = kHalfWB * M * (L + lmax + 1);
+    const int scratch = 48 * kCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
     off_sync = off_tw + 32 * wmax;
-    total = off_sync + (nt == 64 ? 4 * 32 + 16 : 16);  // argmax slots + block id (two warps)
+    total = off_sync + 4 * 32 + 16;  // argmax slots (two warps), block id, sum of weights
   }
 };
 
