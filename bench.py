@@ -150,6 +150,32 @@ def run_reference(args, wl, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def ncu_profile(mode):
+    """DRAM bytes (read + write) per launch of the FSE kernels and their shared-memory
+    wavefront utilisation, from the committed `ncu --set full` summary of this workload
+    (profiles/rNN_ncu_fse_c2_<mode>_summary.csv, written by tools/ncu_summary.py)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(str(ROOT / "profiles" / f"r*_ncu_fse_c2_{mode}_summary.csv")))
+    if not files:
+        return {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    traffic, smem, found = 0.0, [], False
+    with open(files[-1]) as f:
+        rows = list(csv.DictReader(f))
+    for r in rows:
+        if "kernel" not in r or "fse" not in r["kernel"]:
+            continue
+        if r["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            traffic += float(r["value"]) * scale.get(r["unit"], 1)
+            found = True
+        if r["metric"] == "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed":
+            smem.append(round(float(r["value"]), 1))
+    if not found:
+        return {}
+    return {"traffic": int(traffic), "smem_pct": smem, "source": Path(files[-1]).name}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -293,9 +319,12 @@ def main():
     st = res["stats"]
     mean_k = res["fse_ms"]
     achieved = st.flops_executed / (mean_k * 1e-3) / 1e12
+    prof = ncu_profile(args.mode)
     roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64.value, 3),
             "unit": "TFLOP/s", "frac": round(achieved / fp64.value, 4),
-            "traffic": None,
+            "traffic": prof.get("traffic"),
+            "traffic_source": prof.get("source"),
+            "smem_wavefront_pct_of_peak_ncu": prof.get("smem_pct"),
             "peak_source": "FP64 DFMA rate measured live by tf_calibrate (MEASURED_PEAKS.json has no FP64 figure)",
             "fse_kernel_ms": round(mean_k, 4), "flops_executed_per_launch": st.flops_executed,
             "flops_algorithmic_per_launch": st.flops,
