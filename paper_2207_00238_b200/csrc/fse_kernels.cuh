@@ -119,7 +119,13 @@ struct WarpLayout {
 #ifndef TF_HALF_W32
 #define TF_HALF_W32 0  // 1: half kernels keep W as FP32 complex (8 B); 2: also the correction in FP32
 #endif
-constexpr int kHalfWB = TF_HALF_W32 ? 8 : 16;  // bytes per W element in the half kernels
+#ifndef TF_HALF_ACC32
+#define TF_HALF_ACC32 0  // 1: FP32 correction accumulators + FP32 keys, FP64 R refreshed periodically
+#endif
+#ifndef TF_HALF_REFRESH
+#define TF_HALF_REFRESH 8  // iterations between FP64 refreshes (power of two)
+#endif
+constexpr int kHalfWB = (TF_HALF_W32 || TF_HALF_ACC32) ? 8 : 16;  // bytes per W element
 
 struct HalfLayout {
   int wbytes, off_tw, off_sync, total;
