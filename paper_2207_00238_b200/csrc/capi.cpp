@@ -125,6 +125,7 @@ struct Gpu {
   int occ_smem[2][tfb::kNumCfgs] = {};
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
+  bool fft_ok = false;        // c_fft32 uploaded on this device
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
@@ -195,6 +196,10 @@ static int upload_tables(Gpu& g, const tf_fse_params& p, int wmax, cudaStream_t 
   TF_CUDA(cudaMemcpyAsync(g.rho.p, rho.data(), n_rho * sizeof(double), cudaMemcpyHostToDevice, s));
   TF_CUDA(cudaMemcpyAsync(g.tw.p, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   TF_CUDA(cudaStreamSynchronize(s));  // pageable sources: keep them alive until copied
+  if (tw_n >= 32 && !g.fft_ok) {  // constant-memory FFT twiddles (per device, once)
+    TF_CUDA(tfb::fft_tables_upload(tw.data() + 2 * (32 * 31 / 2)));
+    g.fft_ok = true;
+  }
   g.rho_val = p.rho;
   g.rho_margin = p.margin;
   g.tw_wmax = tw_n;
@@ -272,12 +277,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                       int part, int n_parts, uint8_t* d_out, cudaStream_t s, bool want_stats,
                       DevRun* res) {
   const bool exact = ctx->mode == TF_MODE_EXACT;
-  const int cfg = tfb::pick_config(pl.nmax);
+  // bins the CTA kernel's threads carry: the full window, or FAST's Hermitian half
+  const bool half = tfb::cta_half(exact);
+  const int ncarry = half ? (pl.wmax / 2 + 1) * pl.wmax : pl.nmax;
+  const int cfg = tfb::pick_config(ncarry);
   if (cfg < 0)
     return set_error(TF_EUNSUPPORTED, "support window of " + std::to_string(pl.nmax) +
                                           " bins exceeds the kernel capacity (8192)");
   const int nt = tfb::kCfgs[cfg].nt, nb = nt * tfb::kCfgs[cfg].bpt;
-  const tfb::SmemLayout lay(nb, pl.wmax, p.iters, nt / 32);
+  const tfb::SmemLayout lay(nb, pl.wmax, p.iters, nt / 32, half ? pl.wmax * pl.wmax : nb);
   if (lay.total > 227 * 1024)
     return set_error(TF_EUNSUPPORTED, "shared-memory footprint " + std::to_string(lay.total) +
                                           " B exceeds 227 KB");
@@ -485,6 +493,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     // runs the row pass fully, the column pass / update / argmax on rows l <= L/2 only and
     // evaluates from the log: 8 M^2 L + 16 Nh L + Nh (11 I_b + 8 P_b) + 11 U_b I_b,
     // Nh = rows carried * M (T_b there is reported as I_b + P_b, an upper bound).
+    // The FAST CTA-list kernels (GEN half warp kernel, or the half-spectrum CTA kernel) carry
+    // Nh = (L/2 + 1) M bins: 8 M^2 L + 16 Nh L + Nh (11 I_b + 8 P_b) + eval (GEN: 11 U_b I_b
+    // from the log; CTA: 14 U_b T_b from the model).
     double fl = 0.0, xfl = 0.0;
     for (size_t q = 0; q < st.size(); ++q) {
       const BlockStat& b = st[q];
@@ -492,10 +503,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       const double f = 2.0 * (4.0 * N * b.M + 8.0 * N * b.L) + 3.0 * N * b.iters +
                        8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
       fl += f;
-      if (wkind == 2 && q >= static_cast<size_t>(cnt[0])) {
+      const bool warp_list = q >= static_cast<size_t>(cnt[0]);
+      if (wkind == 2 && warp_list) {
         const double Nh = static_cast<double>(wbpt) * 32.0;
         xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
                11.0 * b.evaluated * b.iters;
+      } else if (!warp_list && (gbpth || half)) {
+        const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
+        xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
+               (gbpth ? 11.0 * b.evaluated * b.iters : 14.0 * b.evaluated * b.touched);
       } else {
         xfl += f;
       }

@@ -76,18 +76,26 @@ constexpr int kCY = 4;  // rows per DFT chunk
 //         | loop phase {selection log: double2 x iters, int32 x iters}
 //   after the loop the W region holds the model {mval: double2 x cap; lst: int32 x cap;
 //   pos: int16 x nb} (cap = min(2I, nb) distinct touched bins).
+#ifndef TF_CTA_HALF
+#define TF_CTA_HALF 1  // FAST CTA kernel carries the Hermitian half spectrum (rows l <= L/2)
+#endif
+__host__ __device__ constexpr bool cta_half(bool exact) { return !exact && TF_CTA_HALF; }
+
 struct SmemLayout {
   int nb, wmax, iters, nw, cap;
   int off_tw, off_union, off_pix, off_kn, off_lst, off_slots, off_misc, total;
   __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
-  __host__ __device__ SmemLayout(int nb_, int wmax_, int iters_, int nw_)
+  // nf = bins of the full window (W, window bytes, model); nb = bins the threads carry
+  // (== nf except for the FAST half-spectrum CTA kernel)
+  __host__ __device__ SmemLayout(int nb_, int wmax_, int iters_, int nw_, int nf = 0)
       : nb(nb_), wmax(wmax_), iters(iters_), nw(nw_) {
-    cap = iters >= (nb + 1) / 2 ? nb : 2 * iters;
-    off_tw = 32 * nb;
+    if (nf < nb) nf = nb;
+    cap = iters >= (nf + 1) / 2 ? nf : 2 * iters;
+    off_tw = 32 * nf;
     off_union = off_tw + align16(2 * 16 * wmax);
     off_pix = off_union + 48 * kCY * wmax;
-    off_kn = off_pix + nb;
-    const int dft_end = off_kn + nb;
+    off_kn = off_pix + nf;
+    const int dft_end = off_kn + nf;
     off_lst = off_union + 16 * iters;  // int32 log after the double2 log
     const int loop_end = off_lst + 4 * iters;
     off_slots = align16(dft_end > loop_end ? dft_end : loop_end);
@@ -145,12 +153,14 @@ struct HalfLayout {
 struct KernelCfg {
   int nt, bpt;
 };
-constexpr int kNumCfgs = 9;
+constexpr int kNumCfgs = 10;
 extern const KernelCfg kCfgs[kNumCfgs];
 int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                        cudaStream_t s);
+// FFT twiddles (constant memory) from the size-32 cos/sin table: 32 x (cos, sin) of 2 pi j / 32
+cudaError_t fft_tables_upload(const double* tw32);
 cudaError_t div_selftest_launch(long long n, unsigned long long seed, unsigned long long* bad,
                                 cudaStream_t s);
 // warp kernel variants: bins per lane (window M*L = 32*bpt with 32 % M == 0)

@@ -115,10 +115,14 @@ def test_fast_mode_within_tolerance(ctx, fctx):
         assert np.array_equal(ex[~unk], img[~unk])
 
 
-def test_fast_mode_border_windows(ctx, fctx):
+@pytest.mark.parametrize("no_gen", [False, True])
+def test_fast_mode_border_windows(ctx, fctx, no_gen, monkeypatch):
     """Small, odd-sized frames: most windows are clamped by the halo (M, L not powers of two),
-    which the FAST path runs through the GEN half-spectrum kernel."""
-    ds, n = [], 0
+    which the FAST path runs through the GEN half-spectrum warp kernel, or (TF_NO_GEN=1)
+    through the half-spectrum CTA kernel."""
+    if no_gen:
+        monkeypatch.setenv("TF_NO_GEN", "1")
+    ds = []
     for cfg in (2, 3):
         wl = CONFIGS[cfg]
         for (W, H), tiles in (((37, 29), 1), ((61, 44), 2), ((100, 57), 3), ((45, 90), 4)):
