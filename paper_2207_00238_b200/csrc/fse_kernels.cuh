@@ -69,6 +69,10 @@ struct EnumLaunch {
 };
 
 constexpr int kCY = 4;  // rows per DFT chunk
+#ifndef TF_HALF_CY
+#define TF_HALF_CY 4  // 8 measured slower (register spills)
+#endif
+constexpr int kHalfCY = TF_HALF_CY;  // rows per row-DFT chunk of the half kernels
 
 // Shared-memory layout of the FSE kernel (bytes), computed identically on host and device.
 //   [W replicated (2L x M or L x 2M double2, <= 2*nb)][twiddles: double2 x 2*wmax][union][slots][misc]
@@ -140,7 +144,7 @@ struct HalfLayout {
   __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt) {
     const int lmax = bpth * (nt / M) - 1;
     const int rows = kHalfWB * M * (L + lmax + 1);
-    const int scratch = 48 * kCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
+    const int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
