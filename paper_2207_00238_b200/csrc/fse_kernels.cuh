@@ -129,7 +129,7 @@ struct WarpLayout {
 // (the gathers touch rows 1..L+lmax only), the DFT scratch above row L until that copy
 // is written; then the twiddles and misc.  lmax = bpth * (32 / M) - 1.
 #ifndef TF_HALF_W32
-#define TF_HALF_W32 2  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 and the rank-2 correction in FP32
+#define TF_HALF_W32 3  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 + FP32 rank-2 correction; 3: as 2 in packed FP32x2
 #endif
 #ifndef TF_HALF_ACC32
 #define TF_HALF_ACC32 0  // 1: FP32 correction accumulators + FP32 keys, FP64 R refreshed periodically
