@@ -148,7 +148,7 @@ struct HalfLayout {
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
-    off_sync = off_tw + 32 * wmax;
+    off_sync = off_tw + 32 * wmax + 24 * wmax;  // FP64 twiddles x/y, FP32 twiddles x/y/y-swapped
     total = off_sync + 4 * 32 + 16;  // argmax slots (two warps), block id, sum of weights
   }
 };
