@@ -177,3 +177,31 @@ def test_exact_mode_full_c2_frame_equals_oracle(ctx):
     got, st = ctx.tiled(img, kn, wl.tiles, wl.overlap, p)
     assert int((got != want).sum()) == 0
     assert st.blocks_reference == int(bpt.sum())
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_partitioned_runs_compose_to_the_full_run(ctx, fctx, mode):
+    """One-process-per-GPU path on one device: the parts t % n_parts == part, run one after
+    another in place, reproduce the single-part output byte-for-byte (runtime.hpp:102)."""
+    import torch
+    c = ctx if mode == "exact" else fctx
+    wl = CONFIGS[2]
+    frames, W, H, tiles = 2, 480, 270, 4
+    imgs, kns = zip(*[T.synth_frame(2, f, W, H) for f in range(frames)])
+    img = torch.from_numpy(np.stack(imgs)).cuda()
+    kn = torch.from_numpy(np.stack(kns)).cuda()
+    full = img.clone()
+    c.tiled_device(full.data_ptr(), kn.data_ptr(), full.data_ptr(), W, H, frames, tiles,
+                   wl.overlap, wl.params)
+    for n_parts in (2, 3):
+        out = img.clone()
+        for part in range(n_parts):
+            c.tiled_device(out.data_ptr(), kn.data_ptr(), out.data_ptr(), W, H, frames, tiles,
+                           wl.overlap, wl.params, part=part, n_parts=n_parts)
+        torch.cuda.synchronize()
+        assert torch.equal(out, full), n_parts
+    if mode == "exact":
+        want, _ = O.tiled(np.stack(imgs), np.stack(kns), tiles, wl.overlap, wl.params.block_size,
+                          wl.params.support_margin, wl.params.model_iterations,
+                          wl.params.compensation, wl.params.weight_decay)
+        assert np.array_equal(full.cpu().numpy(), want)
