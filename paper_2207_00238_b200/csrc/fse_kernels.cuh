@@ -128,6 +128,9 @@ struct WarpLayout {
 // FAST half-spectrum warp kernel layout: W rows 0..L-1 plus a copy of rows 0..lmax
 // (the gathers touch rows 1..L+lmax only), the DFT scratch above row L until that copy
 // is written; then the twiddles and misc.  lmax = bpth * (32 / M) - 1.
+#ifndef TF_HALF_T2
+#define TF_HALF_T2 1  // 32x32 half kernel: y-transform on the 17 half rows first, then x
+#endif
 #ifndef TF_HALF_W32
 #define TF_HALF_W32 3  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 + FP32 rank-2 correction; 3: as 2 in packed FP32x2
 #endif
@@ -144,11 +147,13 @@ struct HalfLayout {
   __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt) {
     const int lmax = bpth * (nt / M) - 1;
     const int rows = kHalfWB * M * (L + lmax + 1);
-    const int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
+    int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
+    if (M == 32 && L == 32 && bpth == 17 && nt == 32 && scratch < 24 * 17 * 32)
+      scratch = 24 * 17 * 32;  // TF_HALF_T2: C(x, l) of the 17 half rows, FP64 values + FP32 weights
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
-    off_sync = off_tw + 32 * wmax + 24 * wmax;  // FP64 twiddles x/y, FP32 twiddles x/y/y-swapped
+    off_sync = off_tw + 32 * wmax + 32 * wmax;  // FP64 twiddles x/y, FP32 x/y/y-swapped/x-swapped
     total = off_sync + 4 * 32 + 16;  // argmax slots (two warps), block id, sum of weights
   }
 };
