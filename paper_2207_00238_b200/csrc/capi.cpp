@@ -506,8 +506,11 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       const bool warp_list = q >= static_cast<size_t>(cnt[0]);
       if (wkind == 2 && warp_list) {
         const double Nh = static_cast<double>(wbpt) * 32.0;
-        xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
-               11.0 * b.evaluated * b.iters;
+        // 32x32 with TF_HALF_T2: y-transform on the half rows (8 M L Lh), then x (16 Nh M)
+        const double dft = (TF_HALF_T2 && b.M == 32 && b.L == 32)
+                               ? 8.0 * b.M * b.L * (b.L / 2 + 1) + 16.0 * Nh * b.M
+                               : 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L;
+        xfl += dft + Nh * (11.0 * b.iters + 8.0 * b.pairs) + 11.0 * b.evaluated * b.iters;
       } else if (!warp_list && (gbpth || half)) {
         const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
         xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
