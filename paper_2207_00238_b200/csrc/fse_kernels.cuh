@@ -148,8 +148,8 @@ struct HalfLayout {
     const int lmax = bpth * (nt / M) - 1;
     const int rows = kHalfWB * M * (L + lmax + 1);
     int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
-    if (M == 32 && L == 32 && bpth == 17 && nt == 32 && scratch < 24 * 17 * 32)
-      scratch = 24 * 17 * 32;  // TF_HALF_T2: C(x, l) of the 17 half rows, FP64 values + FP32 weights
+    if (nt == 32 && M == L && scratch < 24 * bpth * 32)
+      scratch = 24 * bpth * 32;  // TF_HALF_T2: C(x, l) of the half rows, FP64 values + FP32 weights
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
