@@ -69,6 +69,15 @@ def build_oracle(with_ref: bool | None = None) -> None:
         subprocess.run(["make", "-s", "-C", str(odir), "ref", f"REF_INCLUDE={ref_inc}"], check=True)
 
 
+def build_integration() -> None:
+    """The reference's run_master driving GPU workers (integration/): built
+    only where the reference headers exist; the binary travels to the GPU box."""
+    ref_inc = Path(os.environ.get("TF_REF_INCLUDE", "/root/reference/proj/include"))
+    if ref_inc.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "integration"), f"REF_INCLUDE={ref_inc}"],
+                       check=True)
+
+
 if __name__ == "__main__":
     if "--variant" in sys.argv:  # --variant NAME DEF1 DEF2 ... (tuning builds under _lib/variants/)
         i = sys.argv.index("--variant")
@@ -78,4 +87,5 @@ if __name__ == "__main__":
     build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
     if "--oracle" in sys.argv:
         build_oracle()
+        build_integration()
     print(LIB)
