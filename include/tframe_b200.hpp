@@ -8,6 +8,7 @@
 // else (CUDA, NCCL) throws tfb200::Error.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -59,18 +60,30 @@ class Context {
   std::unique_ptr<tf_ctx, void (*)(tf_ctx*)> h_;
 };
 
-// FseLiteExtrapolator (extrapolate.hpp:390-414) computed on B200s.  Images are
-// row-major u8 (stride = width); masks u8, nonzero = known.
-class FseLiteExtrapolator {
+// Extrapolator (extrapolate.hpp:22-36): images are row-major u8 (stride = width), masks
+// u8 with nonzero = known; the output keeps every known pixel.
+class Extrapolator {
+ public:
+  virtual ~Extrapolator() = default;
+  virtual std::string name() const = 0;
+  virtual int influence_radius() const = 0;
+  virtual std::string params_string() const = 0;
+  virtual std::vector<uint8_t> extrapolate(const std::vector<uint8_t>& image,
+                                           const std::vector<uint8_t>& known, int width,
+                                           int height) const = 0;
+};
+
+// FseLiteExtrapolator (extrapolate.hpp:390-414) computed on B200s.
+class FseLiteExtrapolator : public Extrapolator {
  public:
   explicit FseLiteExtrapolator(FseLiteParams p = {}, std::shared_ptr<Context> ctx = nullptr)
       : p_(p), ctx_(ctx ? std::move(ctx) : std::make_shared<Context>()) {
     const tf_fse_params c = p_.c();
     check(tf_check_fse_params(&c));
   }
-  std::string name() const { return "fse-lite"; }
-  int influence_radius() const { return p_.block_size + p_.support_margin; }
-  std::string params_string() const {
+  std::string name() const override { return "fse-lite"; }
+  int influence_radius() const override { return p_.block_size + p_.support_margin; }
+  std::string params_string() const override {
     char buf[256];
     const tf_fse_params c = p_.c();
     check(tf_fse_params_to_string(&c, buf, sizeof buf));
@@ -78,7 +91,7 @@ class FseLiteExtrapolator {
   }
   const FseLiteParams& params() const { return p_; }
   std::vector<uint8_t> extrapolate(const std::vector<uint8_t>& image, const std::vector<uint8_t>& known,
-                                   int width, int height) const {
+                                   int width, int height) const override {
     if (image.size() != known.size() || image.size() != static_cast<size_t>(width) * height)
       throw std::invalid_argument("fse_lite_extrapolate: image/mask dimension mismatch");
     std::vector<uint8_t> out(image.size());
@@ -92,6 +105,37 @@ class FseLiteExtrapolator {
   std::shared_ptr<Context> ctx_;
 };
 
+// DiffusionExtrapolator (extrapolate.hpp:371-386, diffusion_extrapolate :41-84) on B200s,
+// byte-identical to the reference.
+class DiffusionExtrapolator : public Extrapolator {
+ public:
+  explicit DiffusionExtrapolator(int iterations = 32, std::shared_ptr<Context> ctx = nullptr)
+      : iters_(iterations), ctx_(ctx ? std::move(ctx) : std::make_shared<Context>()) {
+    if (iters_ < 1) throw std::invalid_argument("diffusion_extrapolate: iterations must be >= 1");
+  }
+  std::string name() const override { return "diffusion"; }
+  int influence_radius() const override { return iters_; }
+  std::string params_string() const override { return "iters=" + std::to_string(iters_); }
+  std::vector<uint8_t> extrapolate(const std::vector<uint8_t>& image, const std::vector<uint8_t>& known,
+                                   int width, int height) const override {
+    if (image.size() != known.size() || image.size() != static_cast<size_t>(width) * height)
+      throw std::invalid_argument("diffusion_extrapolate: image/mask dimension mismatch");
+    std::vector<uint8_t> out(image.size());
+    check(tf_diffusion_extrapolate(ctx_->get(), image.data(), known.data(), width, height, iters_,
+                                   out.data()));
+    return out;
+  }
+
+ private:
+  int iters_;
+  std::shared_ptr<Context> ctx_;
+};
+
+// registry_lookup(name, "key=value,...") (extrapolate.hpp:418-437) for both algorithms.
+inline std::unique_ptr<Extrapolator> make_extrapolator(const std::string& name,
+                                                       const std::string& params = "",
+                                                       std::shared_ptr<Context> ctx = nullptr);
+
 // registry_lookup("fse-lite", "key=value,...") (extrapolate.hpp:418-437)
 inline FseLiteExtrapolator registry_lookup(const std::string& name, const std::string& params = "",
                                            std::shared_ptr<Context> ctx = nullptr) {
@@ -100,6 +144,29 @@ inline FseLiteExtrapolator registry_lookup(const std::string& name, const std::s
   tf_fse_params c{};
   check(tf_fse_params_from_string(params.c_str(), &c));
   return FseLiteExtrapolator(FseLiteParams{c.block, c.margin, c.iters, c.gamma, c.rho}, std::move(ctx));
+}
+
+inline std::unique_ptr<Extrapolator> make_extrapolator(const std::string& name,
+                                                       const std::string& params,
+                                                       std::shared_ptr<Context> ctx) {
+  if (name == "diffusion") {
+    // detail::parse_params + param_int("iters", 32) (extrapolate.hpp:344-362, 421-424)
+    int iters = 32;
+    size_t pos = 0;
+    while (pos <= params.size()) {
+      const size_t end = std::min(params.find(',', pos), params.size());
+      const std::string item = params.substr(pos, end - pos);
+      if (!item.empty()) {
+        const size_t eq = item.find('=');
+        if (eq == std::string::npos)
+          throw std::invalid_argument("bad parameter item '" + item + "', expected key=value");
+        if (item.substr(0, eq) == "iters") iters = std::stoi(item.substr(eq + 1));
+      }
+      pos = end + 1;
+    }
+    return std::make_unique<DiffusionExtrapolator>(iters, std::move(ctx));
+  }
+  return std::make_unique<FseLiteExtrapolator>(registry_lookup(name, params, std::move(ctx)));
 }
 
 // run_master (runtime.hpp:75-139): plan -> expand -> FSE per halo -> crop -> merge on the

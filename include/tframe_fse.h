@@ -18,6 +18,8 @@
  *     fse_lite_extrapolate             extrapolate.hpp:263 tf_fse_extrapolate
  *   run_master / run_local             runtime.hpp:75,142 tf_tiled_extrapolate
  *   (blocks processed, FseLiteTrace::residual_energy.size()) tf_count_blocks
+ *   diffusion_extrapolate              extrapolate.hpp:41-84 tf_diffusion_extrapolate
+ *   run_master(algo "diffusion")       runtime.hpp:75       tf_tiled_diffusion
  *
  * Conventions: plain C, caller-owned buffers, no exceptions cross the
  * boundary.  Images are 8-bit row-major (stride = width, frames stacked);
@@ -148,6 +150,17 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img,
                                 const uint8_t* d_known, int W, int H, int frames, int tiles,
                                 int overlap, const tf_fse_params* p, int part, int n_parts,
                                 uint8_t* d_out, void* stream, tf_run_stats* stats);
+
+/* ---- diffusion extrapolator ---------------------------------
+ * DiffusionExtrapolator::extrapolate / diffusion_extrapolate (extrapolate.hpp:41-84,
+ * 367-386): K Jacobi sweeps of the 4-neighbour mean over the unknown pixels, byte-identical
+ * to the reference.  iters < 1 -> TF_EINVAL ("diffusion_extrapolate: iterations must be >= 1"). */
+int tf_diffusion_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int w, int h,
+                             int iters, uint8_t* out);
+/* run_master with algo "diffusion" (runtime.hpp:75-139): per-halo sweeps, cores merged. */
+int tf_tiled_diffusion(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                       int frames, int tiles, int overlap, int iters, uint8_t* out,
+                       tf_run_stats* stats);
 
 /* ---- measurement ----------------------------------------------------------- */
 /* Device durations (ms) of the most recent FSE kernel launches on GPU `gpu`

@@ -30,6 +30,7 @@ int main(int argc, char** argv) {
   }
   const int workers = argc > 4 ? std::atoi(argv[4]) : tab[cfg].tiles;
   const bool fast = argc > 5 && std::strcmp(argv[5], "fast") == 0;
+  const bool diffusion = argc > 5 && std::strncmp(argv[5], "diffusion", 9) == 0;  // "diffusion[=K]"
 
   std::vector<uint8_t> px(static_cast<size_t>(W) * H), kn(px.size());
   if (tf_synth_frame(cfg, 0, W, H, px.data(), kn.data()) != TF_OK) return 3;
@@ -41,8 +42,9 @@ int main(int argc, char** argv) {
   tframe::MasterConfig mc;
   mc.tiles = tab[cfg].tiles;
   mc.overlap = tab[cfg].overlap;
-  mc.algo = "fse-lite";
-  mc.algo_params = tab[cfg].params;
+  mc.algo = diffusion ? "diffusion" : "fse-lite";
+  mc.algo_params = diffusion ? std::string("iters=") + (argv[5][9] == '=' ? argv[5] + 10 : "32")
+                             : std::string(tab[cfg].params);
 
   auto timed = [&](tframe::Transport& t) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -77,7 +79,7 @@ int main(int argc, char** argv) {
   std::printf("{\"config\": %d, \"W\": %d, \"H\": %d, \"tiles\": %d, \"workers\": %d, \"mode\": \"%s\", "
               "\"bytes_equal\": %s, \"differ\": %lld, \"within1\": %.6f, \"gpu_workers_s\": %.6f, "
               "\"cpu_workers_s\": %.6f, \"gpu_compute_span_us\": %lld, \"cpu_compute_span_us\": %lld}\n",
-              cfg, W, H, mc.tiles, workers, fast ? "fast" : "exact", differ == 0 ? "true" : "false", differ,
+              cfg, W, H, mc.tiles, workers, diffusion ? "diffusion" : (fast ? "fast" : "exact"), differ == 0 ? "true" : "false", differ,
               unk ? double(within1) / unk : 1.0, gpu.second, cpu.second,
               static_cast<long long>(gpu.first.second.compute_span_us),
               static_cast<long long>(cpu.first.second.compute_span_us));

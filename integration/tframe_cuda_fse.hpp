@@ -19,26 +19,27 @@
 
 namespace tframe {
 
-class CudaFseLiteExtrapolator final : public Extrapolator {
+// Any tfb200 extrapolator ("fse-lite" or "diffusion") behind the reference's interface.
+class CudaExtrapolator final : public Extrapolator {
  public:
-  explicit CudaFseLiteExtrapolator(tfb200::FseLiteExtrapolator impl) : impl_(std::move(impl)) {}
-  std::string name() const override { return impl_.name(); }  // "fse-lite"
-  std::optional<int> influence_radius() const override { return impl_.influence_radius(); }
-  std::string params_string() const override { return impl_.params_string(); }
+  explicit CudaExtrapolator(std::unique_ptr<tfb200::Extrapolator> impl) : impl_(std::move(impl)) {}
+  std::string name() const override { return impl_->name(); }
+  std::optional<int> influence_radius() const override { return impl_->influence_radius(); }
+  std::string params_string() const override { return impl_->params_string(); }
   ImageBuffer extrapolate(const ImageBuffer& image, const PixelMask& mask) const override {
     const auto px = image.samples();
     const auto kn = mask.flags();
-    auto out = impl_.extrapolate({px.begin(), px.end()}, {kn.begin(), kn.end()}, image.width(),
-                                 image.height());
+    auto out = impl_->extrapolate({px.begin(), px.end()}, {kn.begin(), kn.end()}, image.width(),
+                                  image.height());
     return ImageBuffer(image.width(), image.height(), std::move(out));
   }
 
  private:
-  tfb200::FseLiteExtrapolator impl_;
+  std::unique_ptr<tfb200::Extrapolator> impl_;
 };
 
-// run_worker (runtime.hpp:60-73) with "fse-lite" served by the GPU; other algorithms fall
-// back to the reference registry.  One tfb200::Context (streams, device buffers) per worker.
+// run_worker (runtime.hpp:60-73) with both registered algorithms served by the GPU.  One
+// tfb200::Context (streams, device buffers) per worker.
 inline LocalTransport::WorkerLoop cuda_worker_loop(int device = 0, int mode = TF_MODE_EXACT) {
   return [device, mode](WorkerEndpoint& endpoint) {
     auto ctx = std::make_shared<tfb200::Context>(1, std::vector<int>{device}, mode);
@@ -48,12 +49,8 @@ inline LocalTransport::WorkerLoop cuda_worker_loop(int device = 0, int mode = TF
       const auto* assign = std::get_if<AssignMsg>(&msg);
       if (assign == nullptr) throw ProtocolError("worker: expected ASSIGN or SHUTDOWN");
       try {
-        std::unique_ptr<Extrapolator> algo;
-        if (assign->algo == "fse-lite")
-          algo = std::make_unique<CudaFseLiteExtrapolator>(
-              tfb200::registry_lookup(assign->algo, assign->params, ctx));
-        else
-          algo = registry_lookup(assign->algo, assign->params);
+        const auto algo = std::make_unique<CudaExtrapolator>(
+            tfb200::make_extrapolator(assign->algo, assign->params, ctx));
         ImageBuffer result = algo->extrapolate(assign->pixels, assign->mask);
         endpoint.send(encode(ResultMsg{assign->tile_id, std::move(result)}));
       } catch (const std::exception& e) {

@@ -61,6 +61,9 @@ def orc() -> C.CDLL:
         L.orc_tiled.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.POINTER(orc_params), C.c_void_p, C.c_void_p]
         L.orc_check_params.argtypes = [C.POINTER(orc_params)]
+        L.orc_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.orc_tiled_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_int, C.c_void_p]
         _orc = L
     return _orc
 
@@ -93,6 +96,9 @@ def ref() -> C.CDLL:
         L.ref_tiled_allcores.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                          C.c_int, C.c_int, C.c_void_p]
+        L.ref_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.ref_run_local_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              C.c_int, C.c_int, C.c_void_p]
         L.ref_gen_scatter_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_void_p]
         L.ref_make_scene.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_void_p]
         L.ref_psnr.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
@@ -167,6 +173,53 @@ def tiled(img, known, tiles, overlap, block, margin, iters, gamma, rho):
 
 
 # ------------------------------------------------------------------ reference
+def diffusion(img, known, iters):
+    """C restatement of diffusion_extrapolate (extrapolate.hpp:41-84)."""
+    img, known = _u8(img), _u8(known)
+    h, w = img.shape
+    out = np.empty_like(img)
+    rc = orc().orc_diffusion(img.ctypes.data, known.ctypes.data, w, h, iters, out.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def tiled_diffusion(img, known, tiles, overlap, iters):
+    """run_master with the diffusion extrapolator (C restatement); img (frames, H, W) or (H, W)."""
+    img, known = _u8(img), _u8(known)
+    frames = img.shape[0] if img.ndim == 3 else 1
+    H, W = img.shape[-2:]
+    out = img.copy()
+    rc = orc().orc_tiled_diffusion(img.ctypes.data, known.ctypes.data, W, H, frames, tiles, overlap,
+                                   iters, out.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def ref_diffusion(img, known, iters):
+    """The compiled reference's diffusion_extrapolate."""
+    img, known = _u8(img), _u8(known)
+    h, w = img.shape
+    out = np.empty_like(img)
+    rc = ref().ref_diffusion(img.ctypes.data, known.ctypes.data, w, h, iters, out.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out
+
+
+def ref_run_local_diffusion(img, known, tiles, overlap, iters, workers=1):
+    """The reference's run_local with algo "diffusion"."""
+    img, known = _u8(img), _u8(known)
+    H, W = img.shape
+    out = np.empty_like(img)
+    rc = ref().ref_run_local_diffusion(img.ctypes.data, known.ctypes.data, W, H, tiles, overlap, iters,
+                                       workers, out.ctypes.data)
+    if rc:
+        raise OracleError(rc, ref_error())
+    return out
+
+
 def ref_error() -> str:
     return ref().ref_last_error().decode()
 

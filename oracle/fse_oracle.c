@@ -456,3 +456,89 @@ int orc_tiled(const uint8_t* img, const uint8_t* known, int W, int H, int frames
   free(rects);
   return rc;
 }
+
+/* ---- diffusion extrapolator (extrapolate.hpp:41-84): K Jacobi sweeps, unknown pixels start
+ * at 128 and take the mean of their in-bounds 4-neighbours (left, right, up, down summed in
+ * that order, then divided by the count); known pixels fixed; floor(v + 0.5) clamped. */
+int orc_diffusion(const uint8_t* img, const uint8_t* known, int w, int h, int iters,
+                  uint8_t* out) {
+  if (w < 1 || h < 1) return ORC_EINVAL;
+  if (iters < 1) return ORC_EINVAL;
+  const size_t n = (size_t)w * h;
+  double* cur = malloc(sizeof(double) * n);
+  double* nxt = malloc(sizeof(double) * n);
+  if (!cur || !nxt) {
+    free(cur);
+    free(nxt);
+    return ORC_ENOMEM;
+  }
+  for (size_t i = 0; i < n; ++i) cur[i] = known[i] ? (double)img[i] : 128.0;
+  memcpy(nxt, cur, sizeof(double) * n);
+  for (int it = 0; it < iters; ++it) {
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        const size_t i = (size_t)y * w + x;
+        if (known[i]) continue;
+        double sum = 0.0;
+        int cnt = 0;
+        if (x > 0) { sum += cur[i - 1]; ++cnt; }
+        if (x + 1 < w) { sum += cur[i + 1]; ++cnt; }
+        if (y > 0) { sum += cur[i - (size_t)w]; ++cnt; }
+        if (y + 1 < h) { sum += cur[i + (size_t)w]; ++cnt; }
+        nxt[i] = cnt > 0 ? sum / cnt : 128.0;
+      }
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    if (known[i]) {
+      out[i] = img[i];
+    } else {
+      double v = floor(cur[i] + 0.5);
+      v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+      out[i] = (uint8_t)v;
+    }
+  }
+  free(cur);
+  free(nxt);
+  return ORC_OK;
+}
+
+/* run_master with the diffusion extrapolator per halo (runtime.hpp:75-139). */
+int orc_tiled_diffusion(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
+                        int tiles, int overlap, int iters, uint8_t* out) {
+  int32_t* rects = malloc(sizeof(int32_t) * 4 * (size_t)tiles);
+  if (!rects) return ORC_ENOMEM;
+  int rc = orc_plan_proposed(W, H, tiles, rects);
+  for (int f = 0; rc == ORC_OK && f < frames; ++f) {
+    const size_t plane = (size_t)W * H * f;
+    for (int t = 0; rc == ORC_OK && t < tiles; ++t) {
+      int32_t halo[4];
+      rc = orc_expand(&rects[4 * t], overlap, W, H, halo);
+      if (rc != ORC_OK) break;
+      const size_t hn = (size_t)halo[2] * halo[3];
+      uint8_t* si = malloc(hn);
+      uint8_t* sm = malloc(hn);
+      uint8_t* so = malloc(hn);
+      for (int y = 0; y < halo[3]; ++y) {
+        memcpy(si + (size_t)y * halo[2], img + plane + (size_t)(halo[1] + y) * W + halo[0],
+               (size_t)halo[2]);
+        memcpy(sm + (size_t)y * halo[2], known + plane + (size_t)(halo[1] + y) * W + halo[0],
+               (size_t)halo[2]);
+      }
+      rc = orc_diffusion(si, sm, halo[2], halo[3], iters, so);
+      if (rc == ORC_OK) {
+        const int ox = rects[4 * t] - halo[0], oy = rects[4 * t + 1] - halo[1];
+        for (int y = 0; y < rects[4 * t + 3]; ++y)
+          memcpy(out + plane + (size_t)(rects[4 * t + 1] + y) * W + rects[4 * t],
+                 so + (size_t)(oy + y) * halo[2] + ox, (size_t)rects[4 * t + 2]);
+      }
+      free(si);
+      free(sm);
+      free(so);
+    }
+  }
+  free(rects);
+  return rc;
+}

@@ -32,6 +32,11 @@ int orc_fse_lite(const uint8_t* img, const uint8_t* known, int w, int h, const o
                  uint8_t* out, orc_block_stats* stats, int64_t stats_cap, int64_t* n_blocks);
 int orc_tiled(const uint8_t* img, const uint8_t* known, int W, int H, int frames, int tiles,
               int overlap, const orc_params* p, uint8_t* out, int64_t* blocks_per_tile);
+/* diffusion extrapolator (extrapolate.hpp:41-84) and its tiled run (runtime.hpp:75-139) */
+int orc_diffusion(const uint8_t* img, const uint8_t* known, int w, int h, int iters,
+                  uint8_t* out);
+int orc_tiled_diffusion(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
+                        int tiles, int overlap, int iters, uint8_t* out);
 
 #ifdef __cplusplus
 }

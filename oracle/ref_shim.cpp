@@ -274,6 +274,43 @@ int ref_tiled_allcores(const uint8_t* img, const uint8_t* known, int W, int H, i
   }
 }
 
+// diffusion_extrapolate (extrapolate.hpp:41-84) and run_local with algo "diffusion"
+int ref_diffusion(const uint8_t* img, const uint8_t* known, int w, int h, int iters, uint8_t* out) {
+  try {
+    tframe::DiffusionParams p;
+    p.iterations = iters;
+    const auto res = tframe::diffusion_extrapolate(to_image(img, w, h), to_mask(known, w, h), p);
+    std::memcpy(out, res.samples().data(), res.size());
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 9);
+  }
+}
+
+int ref_run_local_diffusion(const uint8_t* img, const uint8_t* known, int W, int H, int tiles,
+                            int overlap, int iters, int workers, uint8_t* out) {
+  try {
+    tframe::MasterConfig cfg;
+    cfg.tiles = tiles;
+    cfg.overlap = overlap;
+    cfg.strategy = tframe::Strategy::proposed;
+    cfg.algo = "diffusion";
+    cfg.algo_params = "iters=" + std::to_string(iters);
+    auto [res, stats] = tframe::run_local(to_image(img, W, H), to_mask(known, W, H), cfg,
+                                          static_cast<size_t>(workers));
+    std::memcpy(out, res.samples().data(), res.size());
+    return 0;
+  } catch (const tframe::TilingError& e) {
+    return fail(e, 4);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 9);
+  }
+}
+
 int ref_gen_scatter_mask(int w, int h, double fraction, int block, uint32_t seed, uint8_t* out) {
   try {
     const auto m = tframe::gen_scatter_mask(w, h, fraction, block, seed);

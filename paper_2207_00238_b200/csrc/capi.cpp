@@ -129,6 +129,7 @@ struct Gpu {
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
+  DevBuf dfield0, dfield1, dfoff, dpoff;        // diffusion: FP64 fields, tile offsets
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
   // ring of (start, stop) events around the most recent FSE kernel launches
   static constexpr int kRing = 256;
@@ -700,38 +701,11 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
   return TF_OK;
 }
 
-int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
-                         int frames, int tiles, int overlap, const tf_fse_params* p, uint8_t* out,
-                         tf_run_stats* stats) {
-  if (!ctx) return set_error(TF_EINVAL, "null context");
-  if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
-  int rc = check_params(p);
-  if (rc != TF_OK) return rc;
-  const auto t0 = clk::now();
-  Plan pl;
-  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
-  if (rc != TF_OK) return rc;
-  const int64_t plan_us = us_since(t0);
+// Gather the cores of GPUs 1..n-1 into GPU 0 (NCCL send/recv over NVLink), download the
+// merged frames from GPU 0 and wait for every GPU (run_master's merge, runtime.hpp:112-130).
+static int gather_download(tf_ctx* ctx, const Plan& pl, int W, int H, size_t bytes, uint8_t* out) {
   const int n = static_cast<int>(ctx->gpus.size());
-  const size_t bytes = static_cast<size_t>(W) * H * frames;
-  // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
-  std::vector<DevRun> dr(static_cast<size_t>(n));
-  for (int gi = 0; gi < n; ++gi) {
-    Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
-    rc = select_device(g);
-    if (rc != TF_OK) return rc;
-    TF_CUDA(g.img.ensure(bytes));
-    TF_CUDA(g.known.ensure(bytes));
-    TF_CUDA(g.out.ensure(bytes));
-    TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
-    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
-    rc = run_device(ctx, g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, *p, gi,
-                    n, g.out.as<uint8_t>(), g.stream, false, nullptr);
-    if (rc != TF_OK) return rc;
-  }
-  const auto t_dispatched = clk::now();
-  const int64_t distribute_us = us_since(t0) - plan_us;
-  // ---- gather the cores of GPUs 1..n-1 into GPU 0 (NCCL send/recv over NVLink)
+  int rc = TF_OK;
   Gpu& root = ctx->gpus[0];
   if (n > 1) {
     Nccl& nc = nccl();
@@ -791,6 +765,42 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     TF_CUDA(cudaSetDevice(ctx->gpus[static_cast<size_t>(gi)].dev));
     TF_CUDA(cudaStreamSynchronize(ctx->gpus[static_cast<size_t>(gi)].stream));
   }
+  return rc;
+}
+
+int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                         int frames, int tiles, int overlap, const tf_fse_params* p, uint8_t* out,
+                         tf_run_stats* stats) {
+  if (!ctx) return set_error(TF_EINVAL, "null context");
+  if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
+  int rc = check_params(p);
+  if (rc != TF_OK) return rc;
+  const auto t0 = clk::now();
+  Plan pl;
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
+  if (rc != TF_OK) return rc;
+  const int64_t plan_us = us_since(t0);
+  const int n = static_cast<int>(ctx->gpus.size());
+  const size_t bytes = static_cast<size_t>(W) * H * frames;
+  // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
+  std::vector<DevRun> dr(static_cast<size_t>(n));
+  for (int gi = 0; gi < n; ++gi) {
+    Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+    rc = select_device(g);
+    if (rc != TF_OK) return rc;
+    TF_CUDA(g.img.ensure(bytes));
+    TF_CUDA(g.known.ensure(bytes));
+    TF_CUDA(g.out.ensure(bytes));
+    TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
+    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+    rc = run_device(ctx, g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, *p, gi,
+                    n, g.out.as<uint8_t>(), g.stream, false, nullptr);
+    if (rc != TF_OK) return rc;
+  }
+  const auto t_dispatched = clk::now();
+  const int64_t distribute_us = us_since(t0) - plan_us;
+  rc = gather_download(ctx, pl, W, H, bytes, out);
+  if (rc != TF_OK) return rc;
   if (stats) {
     *stats = tf_run_stats{};
     stats->plan_us = plan_us;
@@ -817,6 +827,136 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     stats->kernel_ms = kms;
   }
   return TF_OK;
+}
+
+// ---- diffusion extrapolator (extrapolate.hpp:41-84) over the tiled job: this GPU's tiles
+// (t % n_parts == part) -> unknown core pixels of d_out (a copy of d_img is made first).
+static int run_device_diffusion(Gpu& g, const Plan& pl, const uint8_t* d_img, const uint8_t* d_known,
+                                int W, int H, int frames, int iters, int part, int n_parts,
+                                uint8_t* d_out, cudaStream_t s, double* kernel_ms) {
+  std::vector<TileDesc> mine;
+  std::vector<int64_t> foff, poff;
+  int64_t fsum = 0, psum = 0, max_core = 0;
+  int max_halo = 0;
+  for (size_t t = 0; t < pl.tiles.size(); ++t) {
+    if (static_cast<int>(t % static_cast<size_t>(n_parts)) != part) continue;
+    const TileDesc& d = pl.tiles[t];
+    mine.push_back(d);
+    foff.push_back(fsum);
+    poff.push_back(psum);
+    fsum += static_cast<int64_t>(d.hw) * d.hh;
+    psum += static_cast<int64_t>((d.hw + 31) / 32) * ((d.hh + 31) / 32);
+    max_halo = std::max(max_halo, d.hw * d.hh);
+    max_core = std::max<int64_t>(max_core, static_cast<int64_t>(d.cw) * d.ch);
+  }
+  const size_t frame_bytes = static_cast<size_t>(W) * H * frames;
+  if (d_out != d_img)
+    TF_CUDA(cudaMemcpyAsync(d_out, d_img, frame_bytes, cudaMemcpyDeviceToDevice, s));
+  if (mine.empty()) return TF_OK;
+  const size_t nt = mine.size();
+  TF_CUDA(g.tiles.ensure(nt * sizeof(TileDesc)));
+  TF_CUDA(g.dfoff.ensure(nt * sizeof(int64_t)));
+  TF_CUDA(g.dpoff.ensure(nt * sizeof(int64_t)));
+  TF_CUDA(g.dfield0.ensure(static_cast<size_t>(fsum) * sizeof(double)));
+  TF_CUDA(g.dfield1.ensure(static_cast<size_t>(fsum) * sizeof(double)));
+  if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
+  const size_t tb = nt * sizeof(TileDesc), ob = nt * sizeof(int64_t);
+  int rc = ensure_pinned(g, tb + 2 * ob);
+  if (rc != TF_OK) return rc;
+  unsigned char* pin = static_cast<unsigned char*>(g.pinned);
+  std::memcpy(pin, mine.data(), tb);
+  std::memcpy(pin + tb, foff.data(), ob);
+  std::memcpy(pin + tb + ob, poff.data(), ob);
+  TF_CUDA(cudaMemcpyAsync(g.tiles.p, pin, tb, cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaMemcpyAsync(g.dfoff.p, pin + tb, ob, cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaMemcpyAsync(g.dpoff.p, pin + tb + ob, ob, cudaMemcpyHostToDevice, s));
+  TF_CUDA(cudaEventRecord(g.ev_tables, s));
+  TF_CUDA(cudaEventRecord(g.ev0, s));
+  TF_CUDA(tfb::diffusion_launch(d_img, d_known, d_out, W, H, g.tiles.as<TileDesc>(),
+                                static_cast<int>(nt), g.dfoff.as<int64_t>(), g.dpoff.as<int64_t>(),
+                                psum, max_halo, max_core, iters, g.dfield0.as<double>(),
+                                g.dfield1.as<double>(), s));
+  TF_CUDA(cudaEventRecord(g.ev1, s));
+  if (kernel_ms) {
+    TF_CUDA(cudaEventSynchronize(g.ev1));
+    float ms = 0.f;
+    TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+    *kernel_ms = ms;
+  }
+  return TF_OK;
+}
+
+static int check_diffusion(int iters) {
+  if (iters < 1) return set_error(TF_EINVAL, "diffusion_extrapolate: iterations must be >= 1");
+  return TF_OK;
+}
+
+int tf_tiled_diffusion(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                       int frames, int tiles, int overlap, int iters, uint8_t* out,
+                       tf_run_stats* stats) {
+  if (!ctx) return set_error(TF_EINVAL, "null context");
+  if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
+  int rc = check_diffusion(iters);
+  if (rc != TF_OK) return rc;
+  const auto t0 = clk::now();
+  Plan pl;
+  rc = make_plan(W, H, frames, tiles, overlap, 1, 0, pl);  // block grid unused
+  if (rc != TF_OK) return rc;
+  const int64_t plan_us = us_since(t0);
+  const int n = static_cast<int>(ctx->gpus.size());
+  const size_t bytes = static_cast<size_t>(W) * H * frames;
+  for (int gi = 0; gi < n; ++gi) {
+    Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+    rc = select_device(g);
+    if (rc != TF_OK) return rc;
+    TF_CUDA(g.img.ensure(bytes));
+    TF_CUDA(g.known.ensure(bytes));
+    TF_CUDA(g.out.ensure(bytes));
+    TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
+    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+    rc = run_device_diffusion(g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, iters,
+                              gi, n, g.out.as<uint8_t>(), g.stream, nullptr);
+    if (rc != TF_OK) return rc;
+  }
+  const auto t_dispatched = clk::now();
+  const int64_t distribute_us = us_since(t0) - plan_us;
+  // the gather needs g.tiles = the full tile table on every GPU (cores_kernel indexes it)
+  for (int gi = 0; gi < n && n > 1; ++gi) {
+    Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+    rc = select_device(g);
+    if (rc != TF_OK) return rc;
+    TF_CUDA(g.tiles.ensure(pl.tiles.size() * sizeof(TileDesc)));
+    TF_CUDA(cudaMemcpyAsync(g.tiles.p, pl.tiles.data(), pl.tiles.size() * sizeof(TileDesc),
+                            cudaMemcpyHostToDevice, g.stream));
+    TF_CUDA(cudaStreamSynchronize(g.stream));
+  }
+  rc = gather_download(ctx, pl, W, H, bytes, out);
+  if (rc != TF_OK) return rc;
+  if (stats) {
+    *stats = tf_run_stats{};
+    stats->plan_us = plan_us;
+    stats->distribute_us = distribute_us;
+    stats->compute_span_us =
+        std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t_dispatched).count();
+    stats->total_us = us_since(t0);
+    stats->overhead_pixels = pl.overhead;
+    double kms = 0.0;
+    for (int gi = 0; gi < n; ++gi) {
+      Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
+      TF_CUDA(cudaSetDevice(g.dev));
+      float ms = 0.f;
+      TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+      kms = std::max(kms, static_cast<double>(ms));
+    }
+    stats->kernel_ms = kms;
+  }
+  return TF_OK;
+}
+
+int tf_diffusion_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int w, int h,
+                             int iters, uint8_t* out) {
+  // one tile, no overlap: the whole image is the field (extrapolate.hpp:46-84)
+  return tf_tiled_diffusion(ctx, img, known, w, h, 1, 1, 0, iters, out, nullptr);
 }
 
 int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int w, int h,

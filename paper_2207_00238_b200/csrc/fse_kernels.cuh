@@ -168,6 +168,14 @@ int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                        cudaStream_t s);
+// Diffusion extrapolator over the tiles' halos (diffusion.cu).  foff: FP64 field offset of
+// each tile (prefix of hw*hh), poff: 32x32-patch offset of each tile; f0/f1: two fields of
+// sum(hw*hh) doubles.  Writes the unknown core pixels of out.
+cudaError_t diffusion_launch(const uint8_t* img, const uint8_t* known, uint8_t* out, int W, int H,
+                             const TileDesc* tiles, int n_tiles, const int64_t* foff,
+                             const int64_t* poff, int64_t n_patches, int max_halo, int64_t max_core,
+                             int iters, double* f0, double* f1, cudaStream_t s);
+
 // FFT twiddles (constant memory) from the size-32 cos/sin table: 32 x (cos, sin) of 2 pi j / 32
 cudaError_t fft_tables_upload(const double* tw32);
 cudaError_t div_selftest_launch(long long n, unsigned long long seed, unsigned long long* bad,

@@ -194,6 +194,23 @@ class Context:
                                          C.byref(st)))
         return out, RunStats._from_c(st)
 
+    def tiled_diffusion(self, image: np.ndarray, mask: np.ndarray, tiles: int, overlap: int,
+                        iters: int) -> tuple[np.ndarray, "RunStats"]:
+        """run_master with algo "diffusion" (runtime.hpp:75-139)."""
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        kn = np.ascontiguousarray(mask)
+        if kn.dtype != np.uint8:
+            kn = (kn != 0).astype(np.uint8)
+        if img.shape != kn.shape:
+            raise ValueError("run_master: image/mask dimension mismatch")
+        frames, H, W = (1, *img.shape) if img.ndim == 2 else img.shape
+        out = np.empty_like(img)
+        st = N.tf_run_stats()
+        check(lib().tf_tiled_diffusion(self._h, img.ctypes.data, kn.ctypes.data, W, H, frames,
+                                       int(tiles), int(overlap), int(iters), out.ctypes.data,
+                                       C.byref(st)))
+        return out, RunStats._from_c(st)
+
     # -- device path (inputs already in HBM; torch tensors or raw pointers)
     def tiled_device(self, d_img: int, d_known: int, d_out: int, W: int, H: int, frames: int,
                      tiles: int, overlap: int, params: FseLiteParams, stream: int = 0,
@@ -271,6 +288,66 @@ class FseLiteExtrapolator(Extrapolator):
         return out
 
 
+class DiffusionExtrapolator(Extrapolator):
+    """extrapolate.hpp:371-386 (diffusion_extrapolate, :41-84), computed on a B200:
+    byte-identical to the reference."""
+
+    def __init__(self, iterations: int = 32, device: int = 0):
+        if iterations < 1:
+            raise ValueError("diffusion_extrapolate: iterations must be >= 1")
+        self._iters = int(iterations)
+        self._device = device
+
+    def name(self) -> str:
+        return "diffusion"
+
+    def influence_radius(self) -> int:
+        return self._iters
+
+    def params_string(self) -> str:
+        return f"iters={self._iters}"
+
+    def extrapolate(self, image: np.ndarray, mask: np.ndarray) -> np.ndarray:
+        img = np.ascontiguousarray(image, dtype=np.uint8)
+        kn = np.ascontiguousarray(mask)
+        if kn.dtype != np.uint8:
+            kn = (kn != 0).astype(np.uint8)
+        if img.ndim != 2:
+            raise ValueError("extrapolate expects one (H, W) image")
+        if kn.shape != img.shape:
+            raise ValueError("diffusion_extrapolate: image/mask dimension mismatch")
+        out = np.empty_like(img)
+        ctx = default_context(self._device)
+        check(lib().tf_diffusion_extrapolate(ctx.handle, img.ctypes.data, kn.ctypes.data, img.shape[1],
+                                             img.shape[0], self._iters, out.ctypes.data))
+        return out
+
+
+def _parse_params(s: str) -> dict:
+    """detail::parse_params (extrapolate.hpp:344-356)."""
+    out = {}
+    for item in s.split(","):
+        if not item:
+            continue
+        if "=" not in item:
+            raise ValueError(f"bad parameter item '{item}', expected key=value")
+        k, v = item.split("=", 1)
+        out[k] = v
+    return out
+
+
+def _stoi(v: str) -> int:
+    """std::stoi: optional whitespace and sign, then digits; trailing text ignored."""
+    import re
+    m = re.match(r"\s*([+-]?\d+)", v)
+    if not m:
+        raise ValueError("stoi")
+    x = int(m.group(1))
+    if not -2**31 <= x < 2**31:
+        raise OverflowError("stoi")
+    return x
+
+
 def fse_lite_extrapolate(image: np.ndarray, mask: np.ndarray,
                          params: FseLiteParams | None = None, mode: str = "exact",
                          device: int = 0) -> np.ndarray:
@@ -279,12 +356,12 @@ def fse_lite_extrapolate(image: np.ndarray, mask: np.ndarray,
 
 
 def registry_lookup(name: str, params: str = "", device: int = 0, mode: str = "exact") -> Extrapolator:
-    """extrapolate.hpp:418-437 for the hot-path algorithm."""
+    """extrapolate.hpp:418-437: "fse-lite" (the hot path) and "diffusion" (§8(f)2)."""
     if name == "fse-lite":
         return FseLiteExtrapolator(_params_from_string(params), device, mode)
     if name == "diffusion":
-        raise NotImplementedError("the diffusion extrapolator is not on the B200 hot path "
-                                  "(SURVEY §8(f) 'next')")
+        kv = _parse_params(params)
+        return DiffusionExtrapolator(_stoi(kv["iters"]) if "iters" in kv else 32, device)
     raise ValueError(f"unknown algorithm '{name}', available: diffusion, fse-lite")
 
 
@@ -328,13 +405,13 @@ def run_master(image: np.ndarray, mask: np.ndarray, config: MasterConfig,
                context: Context | None = None) -> tuple[np.ndarray, RunStats]:
     """runtime.hpp:75-139 on the context's GPUs: plan -> expand -> FSE per halo
     -> crop -> merge.  The output is independent of the GPU count."""
-    if config.algo != "fse-lite":
-        registry_lookup(config.algo, config.algo_params)  # raises for unknown / non-hot-path
+    algo = registry_lookup(config.algo, config.algo_params)  # raises for unknown names
     if config.strategy != "proposed":
         raise NotImplementedError(f"strategy '{config.strategy}' is not part of the B200 hot path")
-    params = _params_from_string(config.algo_params)
     ctx = context or default_context()
-    return ctx.tiled(image, mask, config.tiles, config.overlap, params)
+    if isinstance(algo, DiffusionExtrapolator):
+        return ctx.tiled_diffusion(image, mask, config.tiles, config.overlap, algo.influence_radius())
+    return ctx.tiled(image, mask, config.tiles, config.overlap, algo.params())
 
 
 def run_local(image: np.ndarray, mask: np.ndarray, config: MasterConfig,

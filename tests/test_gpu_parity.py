@@ -205,3 +205,31 @@ def test_partitioned_runs_compose_to_the_full_run(ctx, fctx, mode):
                           wl.params.support_margin, wl.params.model_iterations,
                           wl.params.compensation, wl.params.weight_decay)
         assert np.array_equal(full.cpu().numpy(), want)
+
+
+def test_diffusion_random_cases_equal_oracle():
+    """Diffusion extrapolator (§8(f)2) on the GPU == the C restatement (== the reference)."""
+    rng = np.random.default_rng(11)
+    for _ in range(12):
+        h, w = (int(v) for v in rng.integers(1, 90, 2))
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        kn = (rng.random((h, w)) > rng.random()).astype(np.uint8)
+        k = int(rng.integers(1, 40))
+        got = T.DiffusionExtrapolator(k).extrapolate(img, kn)
+        assert np.array_equal(got, O.diffusion(img, kn, k)), (h, w, k)
+    with pytest.raises(ValueError, match="iterations must be >= 1"):
+        T.DiffusionExtrapolator(0)
+
+
+@pytest.mark.parametrize("tiles,overlap,iters,frames", [(1, 0, 32, 1), (4, 32, 32, 2), (8, 6, 17, 1)])
+def test_diffusion_tiled_equals_oracle(tiles, overlap, iters, frames):
+    wl = CONFIGS[2]
+    W, H = 480, 270
+    imgs, kns = zip(*[T.synth_frame(2, f, W, H) for f in range(frames)])
+    img = np.stack(imgs) if frames > 1 else imgs[0]
+    kn = np.stack(kns) if frames > 1 else kns[0]
+    got, _ = T.run_master(img, kn, T.MasterConfig(tiles=tiles, overlap=overlap, algo="diffusion",
+                                                   algo_params=f"iters={iters}"))
+    want = O.tiled_diffusion(img, kn, tiles, overlap, iters)
+    assert np.array_equal(got, want)
+    del wl

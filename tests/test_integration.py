@@ -33,3 +33,14 @@ def test_reference_master_with_gpu_workers_fast_within_tolerance():
     assert r.returncode == 0, r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["within1"] >= 0.999, out
+
+
+@pytest.mark.gpu
+def test_reference_master_with_gpu_diffusion_workers():
+    if not EXE.exists():
+        pytest.skip("integration binary not built")
+    r = subprocess.run([str(EXE), "2", "480", "270", "4", "diffusion=20"], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["bytes_equal"], out

@@ -121,3 +121,22 @@ def test_restatement_block_stats_consistent():
     assert (st["pairs"] <= st["iters"]).all()
     assert (st["touched"] <= st["iters"] + st["pairs"]).all()
     assert (st["min_gap"] >= 0).all()
+
+
+def test_diffusion_restatement_equals_compiled_reference():
+    """oracle/fse_oracle.c orc_diffusion / orc_tiled_diffusion == the reference's
+    diffusion_extrapolate / run_local(algo="diffusion") byte-for-byte."""
+    if not O.have_ref():
+        pytest.skip("compiled reference not available")
+    rng = np.random.default_rng(7)
+    for _ in range(40):
+        h, w = (int(v) for v in rng.integers(1, 48, 2))
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        kn = (rng.random((h, w)) > rng.random()).astype(np.uint8)
+        k = int(rng.integers(1, 50))
+        assert np.array_equal(O.diffusion(img, kn, k), O.ref_diffusion(img, kn, k))
+    img = rng.integers(0, 256, (130, 170), dtype=np.uint8)
+    kn = (rng.random((130, 170)) > 0.3).astype(np.uint8)
+    for tiles, d, k in ((1, 0, 32), (4, 32, 32), (6, 8, 20), (3, 40, 5)):
+        assert np.array_equal(O.tiled_diffusion(img, kn, tiles, d, k),
+                              O.ref_run_local_diffusion(img, kn, tiles, d, k, 2))

@@ -186,3 +186,22 @@ def test_check_params_messages():
         T.check_fse_params(T.FseLiteParams(4, 8, 10, 0.0))
     with pytest.raises(ValueError, match="weight_decay"):
         T.check_fse_params(T.FseLiteParams(4, 8, 10, 0.5, 1.0))
+
+
+def test_registry_diffusion_matches_reference():
+    """registry_lookup("diffusion", params) (extrapolate.hpp:418-424): default 32 sweeps,
+    params_string / influence radius, key=value parsing errors as the reference."""
+    e = T.registry_lookup("diffusion")
+    assert e.name() == "diffusion" and e.influence_radius() == 32 and e.params_string() == "iters=32"
+    e = T.registry_lookup("diffusion", "iters=7,block=3")
+    assert e.influence_radius() == 7 and e.params_string() == "iters=7"
+    assert T.registry_lookup("diffusion", "iters= 9x,,").influence_radius() == 9  # std::stoi
+    with pytest.raises(ValueError, match="expected key=value"):
+        T.registry_lookup("diffusion", "iters")
+    with pytest.raises(ValueError, match="iterations must be >= 1"):
+        T.registry_lookup("diffusion", "iters=0")
+    if O.have_ref():
+        for s in ("", "iters=7,block=3", "iters= 9x,,"):
+            r = O.ref_registry("diffusion", s)
+            assert r["params_string"] == T.registry_lookup("diffusion", s).params_string()
+            assert r["influence"] == T.registry_lookup("diffusion", s).influence_radius()
