@@ -233,3 +233,18 @@ def test_diffusion_tiled_equals_oracle(tiles, overlap, iters, frames):
     want = O.tiled_diffusion(img, kn, tiles, overlap, iters)
     assert np.array_equal(got, want)
     del wl
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_exact_mode_full_config_frame_equals_reference(ctx, cfg):
+    """Full BASELINE frames (c1 512x512, c3 3840x2160 with 8 tiles) byte-identical to the
+    compiled reference run on all host cores (bit-exact band split)."""
+    if not O.have_ref():
+        pytest.skip("compiled reference not available")
+    wl = CONFIGS[cfg]
+    img, kn = T.synth_frame(cfg, 0, wl.W, wl.H)
+    p = wl.params
+    want = O.ref_tiled_allcores(img, kn, wl.tiles, wl.overlap, p.block_size, p.support_margin,
+                                p.model_iterations, p.compensation, p.weight_decay)
+    got, _ = ctx.tiled(img, kn, wl.tiles, wl.overlap, p)
+    assert int((got != want).sum()) == 0
