@@ -126,6 +126,8 @@ struct Gpu {
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
   bool fft_ok = false;        // c_fft32 uploaded on this device
+  int wide_occ[2][65] = {};    // FAST wide kernel occupancy per (FP64 W, window side)
+  int wide_smem[2][65] = {};
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
@@ -318,6 +320,27 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   const int wn = span * span;
   const tfb::WarpLayout wlay(std::max(wn, 32), pl.wmax, p.iters);
   if (wbpt && (!wlay.fits(wn, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = wkind = 0;
+  // FAST, full windows wider than a warp (span in (32, 64]): the wide half-spectrum kernel
+  // (TF_NO_WIDE=1 keeps them on the CTA kernel); border windows stay on the CTA kernel
+  // W64 (default): W and the update in FP64 — the clustered-loss windows of config 5 are
+  // ill-conditioned enough that the FP32-W variant (TF_WIDE_W32=1) leaves the tolerance there
+  int wide = 0, wide_smem = 0;
+  const bool w64 = !std::getenv("TF_WIDE_W32");
+  if (!nowarp && !exact && !wkind && tfb::wide_supported(span) && !std::getenv("TF_NO_WIDE")) {
+    const tfb::WideLayout wl(span, p.iters, w64);
+    if (wl.total <= 227 * 1024) {
+      if (g.wide_smem[w64][span] != wl.total) {
+        int occ = 0;
+        TF_CUDA(tfb::fse_wide_prepare(span, w64, wl.total, &occ));
+        g.wide_occ[w64][span] = occ;
+        g.wide_smem[w64][span] = wl.total;
+      }
+      if (g.wide_occ[w64][span] >= 1) {
+        wide = span;
+        wide_smem = wl.total;
+      }
+    }
+  }
   // FAST half kernel: W rows + partial copy, log (20 B/iteration) reuses W's space after the loop
   const tfb::HalfLayout hlay(span, span, std::max(wbpt, 1), pl.wmax, hnt);
   if (wkind == 2 && (20 * p.iters > hlay.wbytes || hlay.total > 227 * 1024)) wbpt = wkind = 0;
@@ -349,9 +372,11 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   const int gsmem = gbpth ? tfb::HalfLayout(32, span, gbpth, std::max(pl.wmax, 32), 32).total : 0;
   if (std::getenv("TF_VERBOSE"))
     std::fprintf(stderr,
-                 "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d\n",
+                 "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d"
+                 " | wide %d smem %d occ %d\n",
                  nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
-                 wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0);
+                 wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0, wide,
+                 wide_smem, wide ? g.wide_occ[w64][wide] : 0);
   int rc = upload_tables(g, p, pl.wmax, s);
   if (rc != TF_OK) return rc;
 
@@ -392,8 +417,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   e.n_blocks = g.counters.as<int32_t>();
   e.ref_blocks = g.refblk.as<unsigned long long>();
   e.margin = p.margin;
-  e.warp_M = wbpt ? span : 0;
-  e.warp_L = wbpt ? span : 0;
+  e.warp_M = (wbpt || wide) ? span : 0;
+  e.warp_L = (wbpt || wide) ? span : 0;
   e.wblocks = g.wblocks.as<BlockDesc>();
   e.n_wblocks = g.counters.as<int32_t>() + 2;
   TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
@@ -426,7 +451,25 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   TF_CUDA(cudaEventRecord(g.ev0, s));
   TF_CUDA(cudaEventRecord(g.ring0[slot], s));
   const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
-  if (wbpt) {
+  if (wide) {
+    // border windows (CTA kernel) on a forked stream, concurrently with the wide kernel
+    TF_CUDA(cudaEventRecord(g.ev_fork, s));
+    TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
+    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
+    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
+    const int wgrid = g.sms * g.wide_occ[w64][wide];
+    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(int32_t)));
+    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(double2)));
+    tfb::FseLaunch w = a;
+    w.blocks = g.wblocks.as<BlockDesc>();
+    w.n_blocks = g.counters.as<int32_t>() + 2;
+    w.next_block = g.counters.as<int32_t>() + 3;
+    w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
+    w.wlog_kl = g.wlog_kl.as<int32_t>();
+    w.wlog_c = g.wlog_c.as<double2>();
+    TF_CUDA(tfb::fse_wide_launch(wide, w64, w, wgrid, wide_smem, s));
+    TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
+  } else if (wbpt) {
     // border windows (CTA kernel) on a forked stream, concurrently with the warp kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
@@ -505,7 +548,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                        8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
       fl += f;
       const bool warp_list = q >= static_cast<size_t>(cnt[0]);
-      if (wkind == 2 && warp_list) {
+      if (wide && warp_list) {
+        // wide kernel: pass 1 over y on the half rows (8 S^2 HR), pass 2 over x (16 Nh S),
+        // loop and evaluation as the half kernel
+        const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
+        xfl += 8.0 * b.M * b.L * (b.L / 2 + 1) + 16.0 * Nh * b.M +
+               Nh * (11.0 * b.iters + 8.0 * b.pairs) + 11.0 * b.evaluated * b.iters;
+      } else if (wkind == 2 && warp_list) {
         const double Nh = static_cast<double>(wbpt) * 32.0;
         // 32x32 with TF_HALF_T2: y-transform on the half rows (8 M L Lh), then x (16 Nh M)
         const double dft = (TF_HALF_T2 && b.M == 32 && b.L == 32)
