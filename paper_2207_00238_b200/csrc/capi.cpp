@@ -126,8 +126,8 @@ struct Gpu {
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
   bool fft_ok = false;        // c_fft32 uploaded on this device
-  int wide_occ[2][65] = {};    // FAST wide kernel occupancy per (FP64 W, window side)
-  int wide_smem[2][65] = {};
+  int wide_occ[3][65] = {};    // FAST wide kernel occupancy per (precision variant, window side)
+  int wide_smem[3][65] = {};
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
@@ -322,10 +322,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   if (wbpt && (!wlay.fits(wn, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = wkind = 0;
   // FAST, full windows wider than a warp (span in (32, 64]): the wide half-spectrum kernel
   // (TF_NO_WIDE=1 keeps them on the CTA kernel); border windows stay on the CTA kernel
-  // W64 (default): W and the update in FP64 — the clustered-loss windows of config 5 are
-  // ill-conditioned enough that the FP32-W variant (TF_WIDE_W32=1) leaves the tolerance there
+  // precision variant (TF_WIDE_WM = 0|1|2): 0 = FP32 weights' DFT, W and update; 1 = FP64
+  // weights' DFT, FP32 W and update; 2 = FP64 throughout.  Measured on the full c4 frame
+  // (within +-1 of EXACT / kernel ms): 0.99932 / 11.7, 0.99986 / 14.8, 0.99994 / 15.9 (the
+  // CTA kernel: 1.0 / 24.6); 1 is the default: the FP32 weights' DFT is the main error source
   int wide = 0, wide_smem = 0;
-  const bool w64 = !std::getenv("TF_WIDE_W32");
+  int w64 = 1;
+  if (const char* e = std::getenv("TF_WIDE_WM")) w64 = std::min(2, std::max(0, std::atoi(e)));
   if (!nowarp && !exact && !wkind && tfb::wide_supported(span) && !std::getenv("TF_NO_WIDE")) {
     const tfb::WideLayout wl(span, p.iters, w64);
     if (wl.total <= 227 * 1024) {

@@ -160,25 +160,26 @@ struct HalfLayout {
 
 // FAST wide kernel (full windows S x S, 32 < S <= 64; fse_wide_kernel): NT threads, thread ->
 // column k = tid mod S, row group tid / S (G = NT / S groups), rows l = group + G j <= S/2.
-// W64 = false: W stored FP32 complex (8 B), weights' DFT in FP32; true: FP64 throughout.
+// wm: 0 = W stored FP32 complex (8 B), weights' DFT in FP32; 1 = weights' DFT in FP64, W
+// stored FP32; 2 = FP64 throughout.
 //   [region: W rows 0..S+HR+G-1 | DFT staging (w, w*v per pixel) | C(x, l) of the half rows |
 //    post-loop selection log]
 //   [twiddles: FP64 (cos, sin) x S, FP32 (cos, -sin) x S, FP32 (sin, cos) x S][slots][misc]
 struct WideLayout {
   int nt, g, hr, bp, rows, region, off_tw, off_slots, off_misc, total;
-  __host__ __device__ static constexpr int threads(int S, bool w64) {
-    return w64 ? (S <= 48 ? 192 : 256) : (S <= 48 ? 96 : 128);
+  __host__ __device__ static constexpr int threads(int S, int wm) {
+    return wm ? (S <= 48 ? 192 : 256) : (S <= 48 ? 96 : 128);
   }
-  __host__ __device__ WideLayout(int S, int iters, bool w64) {
-    nt = threads(S, w64);
+  __host__ __device__ WideLayout(int S, int iters, int wm) {
+    nt = threads(S, wm);
     g = nt / S;
     hr = S / 2 + 1;
     bp = (hr + g - 1) / g;
     rows = S + hr + g;
-    const int eb = w64 ? 16 : 8;
+    const int eb = wm == 2 ? 16 : 8;
     int r = eb * S * rows;                   // W, copy rows included
-    const int stage = (w64 ? 16 : 12) * S * S;  // w + w*v per window pixel
-    const int cx = (w64 ? 32 : 24) * hr * S;    // C(x, l): values double2 + weights
+    const int stage = (wm ? 16 : 12) * S * S;  // w + w*v per window pixel
+    const int cx = (wm ? 32 : 24) * hr * S;    // C(x, l): values double2 + weights
     const int lg = 20 * iters;               // selection log (double2 + int32 per iteration)
     r = r > stage ? r : stage;
     r = r > cx ? r : cx;
@@ -225,8 +226,8 @@ cudaError_t fse_half_launch(int nt, int bpth, const FseLaunch& a, int grid, int 
                                  cudaStream_t s);
 // FAST wide kernel for full S x S windows, S in {40, 44, 48, 56, 64} (0 = no variant)
 int wide_supported(int S);
-cudaError_t fse_wide_prepare(int S, bool w64, int smem_bytes, int* ctas_per_sm);
-cudaError_t fse_wide_launch(int S, bool w64, const FseLaunch& a, int grid, int smem_bytes,
+cudaError_t fse_wide_prepare(int S, int wm, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_wide_launch(int S, int wm, const FseLaunch& a, int grid, int smem_bytes,
                             cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,

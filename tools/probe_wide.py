@@ -17,8 +17,8 @@ for c in cfgs:
     kn = np.stack(kns) if wl.frames > 1 else kns[0]
     ex, st_e = ex_ctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
     res = {}
-    for tag, env in (("cta", {"TF_NO_WIDE": "1"}), ("w32", {"TF_WIDE_W32": "1"}), ("w64", {})):
-        for k in ("TF_NO_WIDE", "TF_WIDE_W32"):
+    for tag, env in (("cta", {"TF_NO_WIDE": "1"}), ("wm0", {"TF_WIDE_WM": "0"}), ("wm1", {"TF_WIDE_WM": "1"}), ("wm2", {"TF_WIDE_WM": "2"})):
+        for k in ("TF_NO_WIDE", "TF_WIDE_WM"):
             os.environ.pop(k, None)
         os.environ.update(env)
         best = None
