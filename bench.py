@@ -338,13 +338,16 @@ def main():
     unk = kn_np == 0
     dd = np.abs(ex_out.astype(int) - fa_out.astype(int))[unk]
 
-    def psnr(a, b):
-        m = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
-        return float("inf") if m == 0 else 10 * np.log10(255.0 ** 2 / m)
+    # PSNR / SSIM against the ground truth on the GPU (tf_quality: bit-identical to metrics.hpp)
+    qe, qf = ctx.quality(np.stack([img_np, img_np]), np.stack([ex_out, fa_out]), np.stack([kn_np, kn_np]))
 
     parity = {"fast_within1_of_exact": round(float((dd <= 1).mean()), 6),
               "fast_max_abs_diff": int(dd.max()) if dd.size else 0,
-              "psnr_exact_db": round(psnr(img_np, ex_out), 4), "psnr_fast_db": round(psnr(img_np, fa_out), 4),
+              "psnr_exact_db": round(qe["psnr"], 4), "psnr_fast_db": round(qf["psnr"], 4),
+              "ssim_exact": round(qe["ssim"], 6), "ssim_fast": round(qf["ssim"], 6),
+              "psnr_missing_exact_db": round(qe["psnr_missing"], 4),
+              "psnr_missing_fast_db": round(qf["psnr_missing"], 4),
+              "metrics_source": "GPU tf_quality (metrics.hpp restated)",
               "tolerance": ">= 0.999 within +-1 and |dPSNR| <= 0.05 dB (north star)"}
     parity["fast_dpsnr_db"] = round(abs(parity["psnr_exact_db"] - parity["psnr_fast_db"]), 5)
     parity["fast_within_tolerance"] = bool(parity["fast_within1_of_exact"] >= 0.999 and parity["fast_dpsnr_db"] <= 0.05)

@@ -162,6 +162,38 @@ int tf_tiled_diffusion(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
                        int frames, int tiles, int overlap, int iters, uint8_t* out,
                        tf_run_stats* stats);
 
+/* ---- image-quality metrics on the GPU (metrics.hpp:12-90) -----
+ * Per frame of a frames x h x w batch (a = reference image, b = test image, known = mask,
+ * nonzero = known, may be NULL).  mse / psnr / mse_missing are bit-identical to the
+ * reference (integer sums, same final expressions); ssim's per-window values are
+ * bit-identical and the mean over windows is summed in a fixed tree (deterministic, within
+ * 1e-12 relative of the reference's sequential sum). */
+typedef struct tf_quality_metrics {
+  double mse;          /* mse(a, b) (metrics.hpp:12-24)                                  */
+  double psnr;         /* psnr_from_mse(mse) (metrics.hpp:47-55); +inf when a == b         */
+  double mse_missing;  /* over pixels with known == 0 (metrics.hpp:27-45); NaN if none      */
+  double psnr_missing; /* psnr_from_mse(mse_missing); NaN if none                         */
+  double ssim;         /* mean 8x8 SSIM (metrics.hpp:58-88); NaN if not asked or w|h < 8   */
+  int64_t n_missing;   /* pixels with known == 0                                         */
+} tf_quality_metrics;
+/* Device buffers on GPU `gpu`, enqueued on `stream` (NULL: the context's stream); returns
+ * after the results are on the host. */
+int tf_quality_device(tf_ctx* ctx, int gpu, const uint8_t* d_a, const uint8_t* d_b,
+                      const uint8_t* d_known, int w, int h, int frames, int want_ssim,
+                      void* stream, tf_quality_metrics* out /* frames */);
+/* Host buffers (copied to GPU 0 of the context). */
+int tf_quality(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, const uint8_t* known, int w,
+               int h, int frames, int want_ssim, tf_quality_metrics* out /* frames */);
+/* The reference's single-image functions on the GPU, same errors (std::invalid_argument ->
+ * TF_EINVAL with the reference's message). */
+int tf_mse(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out);
+int tf_mse_missing(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, const uint8_t* known, int w,
+                   int h, double* out); /* no unknown pixel -> "mse_missing: mask has no unknown pixels" */
+int tf_psnr(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out);
+int tf_ssim(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out);
+  /* w or h < 8 -> "ssim: image smaller than the 8x8 window" */
+double tf_psnr_from_mse(double mse); /* metrics.hpp:47-50 */
+
 /* ---- measurement ----------------------------------------------------------- */
 /* Device durations (ms) of the most recent FSE kernel launches on GPU `gpu`
  * (oldest first, up to max_n; the context keeps the last 256).  Synchronises

@@ -105,6 +105,10 @@ def ref() -> C.CDLL:
         L.ref_psnr.restype = C.c_double
         L.ref_ssim.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.ref_ssim.restype = C.c_double
+        L.ref_mse.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.ref_mse.restype = C.c_double
+        L.ref_mse_missing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                      C.POINTER(C.c_double)]
         _ref = L
     return _ref
 
@@ -328,3 +332,67 @@ def psnr(a, b) -> float:
 def ref_interior_boundary(W, H, N) -> int:
     """tiling.hpp:231 on plan_proposed(W, H, N), via the compiled reference."""
     return int(ref().ref_interior_boundary(W, H, N))
+
+
+# ---- metrics (metrics.hpp:12-88): C restatement and the compiled reference
+def _orc_metrics():
+    L = orc()
+    if not getattr(L, "_metrics_bound", False):
+        L.orc_mse.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.orc_mse.restype = C.c_double
+        L.orc_mse_missing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                      C.POINTER(C.c_double)]
+        L.orc_psnr_from_mse.argtypes = [C.c_double]
+        L.orc_psnr_from_mse.restype = C.c_double
+        L.orc_ssim.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.orc_ssim.restype = C.c_double
+        L._metrics_bound = True
+    return L
+
+
+def mse(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    return _orc_metrics().orc_mse(a.ctypes.data, b.ctypes.data, a.shape[1], a.shape[0])
+
+
+def mse_missing(a, b, known) -> float:
+    a, b, k = _u8(a), _u8(b), _u8((np.asarray(known) != 0).astype(np.uint8))
+    v = C.c_double()
+    rc = _orc_metrics().orc_mse_missing(a.ctypes.data, b.ctypes.data, k.ctypes.data, a.shape[1],
+                                        a.shape[0], C.byref(v))
+    if rc:
+        raise OracleError(rc, "mse_missing: mask has no unknown pixels")
+    return v.value
+
+
+def psnr_from_mse(m) -> float:
+    return _orc_metrics().orc_psnr_from_mse(float(m))
+
+
+def orc_psnr(a, b) -> float:
+    return psnr_from_mse(mse(a, b))
+
+
+def ssim(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    return _orc_metrics().orc_ssim(a.ctypes.data, b.ctypes.data, a.shape[1], a.shape[0])
+
+
+def ref_mse(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    return ref().ref_mse(a.ctypes.data, b.ctypes.data, a.shape[1], a.shape[0])
+
+
+def ref_mse_missing(a, b, known) -> float:
+    a, b, k = _u8(a), _u8(b), _u8((np.asarray(known) != 0).astype(np.uint8))
+    v = C.c_double()
+    rc = ref().ref_mse_missing(a.ctypes.data, b.ctypes.data, k.ctypes.data, a.shape[1], a.shape[0],
+                               C.byref(v))
+    if rc:
+        raise OracleError(rc, ref_error())
+    return v.value
+
+
+def ref_ssim(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    return ref().ref_ssim(a.ctypes.data, b.ctypes.data, a.shape[1], a.shape[0])

@@ -542,3 +542,75 @@ int orc_tiled_diffusion(const uint8_t* img, const uint8_t* known, int W, int H, 
   free(rects);
   return rc;
 }
+
+/* ---------------------------------------------------------------- metrics
+ * metrics.hpp:12-88 restated: binary64 accumulation in raster order, the same
+ * expressions (the checker for the GPU quality kernels). */
+
+double orc_mse(const uint8_t* a, const uint8_t* b, int w, int h) {
+  /* metrics.hpp:12-24 */
+  double sum = 0.0;
+  const size_t n = (size_t)w * h;
+  for (size_t i = 0; i < n; ++i) {
+    const double d = (double)a[i] - (double)b[i];
+    sum += d * d;
+  }
+  return sum / (double)n;
+}
+
+int orc_mse_missing(const uint8_t* a, const uint8_t* b, const uint8_t* known, int w, int h,
+                    double* out) {
+  /* metrics.hpp:27-45: pixels the mask marks unknown; none -> error */
+  double sum = 0.0;
+  size_t n = 0;
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const size_t i = (size_t)y * w + x;
+      if (known[i]) continue;
+      const double d = (double)a[i] - (double)b[i];
+      sum += d * d;
+      ++n;
+    }
+  if (n == 0) return ORC_EINVAL;
+  *out = sum / (double)n;
+  return ORC_OK;
+}
+
+double orc_psnr_from_mse(double m) {
+  /* metrics.hpp:47-50 */
+  if (m == 0.0) return INFINITY;
+  return 10.0 * log10(255.0 * 255.0 / m);
+}
+
+double orc_ssim(const uint8_t* a, const uint8_t* b, int w, int h) {
+  /* metrics.hpp:58-88: uniform 8x8 windows, stride 1; NaN when smaller than 8x8 */
+  if (w < 8 || h < 8) return NAN;
+  const double c1 = (0.01 * 255.0) * (0.01 * 255.0);
+  const double c2 = (0.03 * 255.0) * (0.03 * 255.0);
+  const double inv_n = 1.0 / (8 * 8);
+  double total = 0.0;
+  size_t windows = 0;
+  for (int wy = 0; wy + 8 <= h; ++wy)
+    for (int wx = 0; wx + 8 <= w; ++wx) {
+      double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+      for (int y = wy; y < wy + 8; ++y)
+        for (int x = wx; x < wx + 8; ++x) {
+          const double va = a[(size_t)y * w + x];
+          const double vb = b[(size_t)y * w + x];
+          sa += va;
+          sb += vb;
+          saa += va * va;
+          sbb += vb * vb;
+          sab += va * vb;
+        }
+      const double mu_a = sa * inv_n;
+      const double mu_b = sb * inv_n;
+      const double var_a = saa * inv_n - mu_a * mu_a;
+      const double var_b = sbb * inv_n - mu_b * mu_b;
+      const double cov = sab * inv_n - mu_a * mu_b;
+      total += ((2.0 * mu_a * mu_b + c1) * (2.0 * cov + c2)) /
+               ((mu_a * mu_a + mu_b * mu_b + c1) * (var_a + var_b + c2));
+      ++windows;
+    }
+  return total / (double)windows;
+}

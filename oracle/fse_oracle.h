@@ -38,6 +38,13 @@ int orc_diffusion(const uint8_t* img, const uint8_t* known, int w, int h, int it
 int orc_tiled_diffusion(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
                         int tiles, int overlap, int iters, uint8_t* out);
 
+/* metrics.hpp:12-88 */
+double orc_mse(const uint8_t* a, const uint8_t* b, int w, int h);
+int orc_mse_missing(const uint8_t* a, const uint8_t* b, const uint8_t* known, int w, int h,
+                    double* out);
+double orc_psnr_from_mse(double m);
+double orc_ssim(const uint8_t* a, const uint8_t* b, int w, int h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -335,4 +335,18 @@ double ref_ssim(const uint8_t* a, const uint8_t* b, int w, int h) {
   return tframe::ssim(to_image(a, w, h), to_image(b, w, h));
 }
 
+double ref_mse(const uint8_t* a, const uint8_t* b, int w, int h) {
+  return tframe::mse(to_image(a, w, h), to_image(b, w, h));
+}
+
+int ref_mse_missing(const uint8_t* a, const uint8_t* b, const uint8_t* known, int w, int h,
+                    double* out) {
+  try {
+    *out = tframe::mse_missing(to_image(a, w, h), to_image(b, w, h), to_mask(known, w, h));
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 1);
+  }
+}
+
 }  // extern "C"

@@ -37,6 +37,11 @@ class tf_run_stats(C.Structure):
                 ("flops_executed", C.c_double)]
 
 
+class tf_quality_metrics(C.Structure):
+    _fields_ = [("mse", C.c_double), ("psnr", C.c_double), ("mse_missing", C.c_double),
+                ("psnr_missing", C.c_double), ("ssim", C.c_double), ("n_missing", C.c_int64)]
+
+
 _u8p = C.POINTER(C.c_uint8)
 _vp = C.c_void_p
 _i = C.c_int
@@ -75,6 +80,13 @@ SIGNATURES = {
     "tf_comm_gather_cores": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp]),
     "tf_core_layout": (_i, [_i, _i, _i, _i, _i, C.POINTER(tf_rect), _vp, _vp, _vp, _vp]),
     "tf_synth_frame": (_i, [_i, _i, _i, _i, _vp, _vp]),
+    "tf_quality_device": (_i, [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, C.POINTER(tf_quality_metrics)]),
+    "tf_quality": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, C.POINTER(tf_quality_metrics)]),
+    "tf_mse": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(C.c_double)]),
+    "tf_mse_missing": (_i, [_vp, _vp, _vp, _vp, _i, _i, C.POINTER(C.c_double)]),
+    "tf_psnr": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(C.c_double)]),
+    "tf_ssim": (_i, [_vp, _vp, _vp, _i, _i, C.POINTER(C.c_double)]),
+    "tf_psnr_from_mse": (C.c_double, [C.c_double]),
 }
 
 _lib = None

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libtframe_b200.so"
-SOURCES = ["fse_kernels.cu", "diffusion.cu", "capi.cpp", "tiling.cpp", "synth.cpp", "calibrate.cu"]
+SOURCES = ["fse_kernels.cu", "diffusion.cu", "metrics.cu", "capi.cpp", "tiling.cpp", "synth.cpp", "calibrate.cu"]
 HEADERS = ["fse_kernels.cuh", "host_internal.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <numbers>
@@ -116,6 +117,7 @@ struct Gpu {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_tables = nullptr;
   DevBuf img, known, out;                       // host-API frame buffers
   DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv;
+  DevBuf qbuf;                                  // quality metrics: sums, SSIM partials
   void* pinned = nullptr;                       // host staging for tables
   size_t pinned_n = 0;
   double rho_val = -1.0;
@@ -685,7 +687,7 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.comm && nccl().ok) nccl().CommDestroy(g.comm);
     for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
                       &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv, &g.wblocks,
-                      &g.wlog_kl, &g.wlog_c})
+                      &g.wlog_kl, &g.wlog_c, &g.qbuf})
       b->release();
     if (g.pinned) cudaFreeHost(g.pinned);
     for (int r = 0; r < Gpu::kRing; ++r) {
@@ -1015,6 +1017,114 @@ int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
                        const tf_fse_params* p, uint8_t* out) {
   // one tile, no overlap: the whole image is the halo (extrapolate.hpp:263)
   return tf_tiled_extrapolate(ctx, img, known, w, h, 1, 1, 0, p, out, nullptr);
+}
+
+double tf_psnr_from_mse(double mse_value) {
+  // metrics.hpp:47-50
+  if (mse_value == 0.0) return std::numeric_limits<double>::infinity();
+  return 10.0 * std::log10(255.0 * 255.0 / mse_value);
+}
+
+int tf_quality_device(tf_ctx* ctx, int gpu, const uint8_t* d_a, const uint8_t* d_b,
+                      const uint8_t* d_known, int w, int h, int frames, int want_ssim,
+                      void* stream, tf_quality_metrics* out) {
+  if (!ctx || gpu < 0 || gpu >= static_cast<int>(ctx->gpus.size()))
+    return set_error(TF_EINVAL, "bad context or gpu index");
+  if (!d_a || !d_b || !out) return set_error(TF_EINVAL, "null buffer");
+  if (w < 1 || h < 1 || frames < 1) return set_error(TF_EINVAL, "image dimensions must be >= 1");
+  Gpu& g = ctx->gpus[static_cast<size_t>(gpu)];
+  int rc = select_device(g);
+  if (rc != TF_OK) return rc;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  const bool ssim = want_ssim && w >= 8 && h >= 8;
+  const int64_t np = ssim ? tfb::ssim_partials(w, h, frames) : 0;
+  const size_t o_sum = 0, o_ssim = 24 * static_cast<size_t>(frames),
+               o_part = o_ssim + 8 * static_cast<size_t>(frames);
+  TF_CUDA(g.qbuf.ensure(o_part + 8 * static_cast<size_t>(np)));
+  unsigned char* q = g.qbuf.as<unsigned char>();
+  TF_CUDA(tfb::quality_launch(d_a, d_b, d_known, w, h, frames, g.sms,
+                              reinterpret_cast<unsigned long long*>(q + o_sum),
+                              ssim ? reinterpret_cast<double*>(q + o_part) : nullptr,
+                              ssim ? reinterpret_cast<double*>(q + o_ssim) : nullptr, s));
+  std::vector<unsigned char> host(o_part);
+  TF_CUDA(cudaMemcpyAsync(host.data(), q, o_part, cudaMemcpyDeviceToHost, s));
+  TF_CUDA(cudaStreamSynchronize(s));
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  const double n = static_cast<double>(static_cast<int64_t>(w) * h);
+  const double nwin = static_cast<double>(static_cast<int64_t>(w - 7) * (h - 7));
+  for (int f = 0; f < frames; ++f) {
+    unsigned long long v[3];
+    std::memcpy(v, host.data() + o_sum + 24 * static_cast<size_t>(f), sizeof(v));
+    double ss = 0.0;
+    std::memcpy(&ss, host.data() + o_ssim + 8 * static_cast<size_t>(f), sizeof(ss));
+    tf_quality_metrics& r = out[f];
+    // integer sums == the reference's exact binary64 sums (every partial sum < 2^53)
+    r.mse = static_cast<double>(v[0]) / n;
+    r.psnr = tf_psnr_from_mse(r.mse);
+    r.n_missing = d_known ? static_cast<int64_t>(v[2]) : 0;
+    r.mse_missing = r.n_missing ? static_cast<double>(v[1]) / static_cast<double>(v[2]) : nan;
+    r.psnr_missing = r.n_missing ? tf_psnr_from_mse(r.mse_missing) : nan;
+    r.ssim = ssim ? ss / nwin : nan;
+  }
+  return TF_OK;
+}
+
+int tf_quality(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, const uint8_t* known, int w,
+               int h, int frames, int want_ssim, tf_quality_metrics* out) {
+  if (!ctx) return set_error(TF_EINVAL, "null context");
+  if (!a || !b || !out) return set_error(TF_EINVAL, "null buffer");
+  if (w < 1 || h < 1 || frames < 1) return set_error(TF_EINVAL, "image dimensions must be >= 1");
+  Gpu& g = ctx->gpus[0];
+  int rc = select_device(g);
+  if (rc != TF_OK) return rc;
+  const size_t bytes = static_cast<size_t>(w) * h * frames;
+  TF_CUDA(g.img.ensure(bytes));
+  TF_CUDA(g.out.ensure(bytes));
+  TF_CUDA(cudaMemcpyAsync(g.img.p, a, bytes, cudaMemcpyHostToDevice, g.stream));
+  TF_CUDA(cudaMemcpyAsync(g.out.p, b, bytes, cudaMemcpyHostToDevice, g.stream));
+  if (known) {
+    TF_CUDA(g.known.ensure(bytes));
+    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+  }
+  return tf_quality_device(ctx, 0, g.img.as<uint8_t>(), g.out.as<uint8_t>(),
+                           known ? g.known.as<uint8_t>() : nullptr, w, h, frames, want_ssim,
+                           nullptr, out);
+}
+
+int tf_mse(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out) {
+  if (!out) return set_error(TF_EINVAL, "null output");
+  tf_quality_metrics q;
+  const int rc = tf_quality(ctx, a, b, nullptr, w, h, 1, 0, &q);
+  if (rc == TF_OK) *out = q.mse;
+  return rc;
+}
+
+int tf_mse_missing(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, const uint8_t* known, int w,
+                   int h, double* out) {
+  if (!out || !known) return set_error(TF_EINVAL, "null buffer");
+  tf_quality_metrics q;
+  const int rc = tf_quality(ctx, a, b, known, w, h, 1, 0, &q);
+  if (rc != TF_OK) return rc;
+  if (q.n_missing == 0) return set_error(TF_EINVAL, "mse_missing: mask has no unknown pixels");
+  *out = q.mse_missing;
+  return TF_OK;
+}
+
+int tf_psnr(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out) {
+  if (!out) return set_error(TF_EINVAL, "null output");
+  tf_quality_metrics q;
+  const int rc = tf_quality(ctx, a, b, nullptr, w, h, 1, 0, &q);
+  if (rc == TF_OK) *out = q.psnr;
+  return rc;
+}
+
+int tf_ssim(tf_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, double* out) {
+  if (!out) return set_error(TF_EINVAL, "null output");
+  if (w < 8 || h < 8) return set_error(TF_EINVAL, "ssim: image smaller than the 8x8 window");
+  tf_quality_metrics q;
+  const int rc = tf_quality(ctx, a, b, nullptr, w, h, 1, 1, &q);
+  if (rc == TF_OK) *out = q.ssim;
+  return rc;
 }
 
 int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* cores,

@@ -229,6 +229,13 @@ int wide_supported(int S);
 cudaError_t fse_wide_prepare(int S, int wm, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_wide_launch(int S, int wm, const FseLaunch& a, int grid, int smem_bytes,
                             cudaStream_t s);
+// Quality metrics (metrics.cu): per frame sse3[3f..3f+2] = {sum d^2, sum over unknown d^2,
+// unknown count} (known may be null); with partial (ssim_partials doubles) and ssim_sum
+// (frames doubles), the per-frame sum of the 8x8 window SSIM values.
+int64_t ssim_partials(int w, int h, int frames);
+cudaError_t quality_launch(const uint8_t* a, const uint8_t* b, const uint8_t* known, int w, int h,
+                           int frames, int sms, unsigned long long* sse3, double* partial,
+                           double* ssim_sum, cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,

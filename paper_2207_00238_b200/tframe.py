@@ -211,6 +211,36 @@ class Context:
                                        C.byref(st)))
         return out, RunStats._from_c(st)
 
+    # -- quality metrics (metrics.hpp:12-90) on the GPU
+    def quality(self, a: np.ndarray, b: np.ndarray, mask: np.ndarray | None = None,
+                ssim: bool = True) -> list[dict]:
+        """Per frame of (H, W) or (F, H, W) u8 images: mse, psnr, mse_missing,
+        psnr_missing, ssim, n_missing (tf_quality in include/tframe_fse.h)."""
+        A = np.ascontiguousarray(a, dtype=np.uint8)
+        B = np.ascontiguousarray(b, dtype=np.uint8)
+        if A.shape != B.shape:
+            raise ValueError("mse: dimension mismatch")
+        frames, H, W = (1, *A.shape) if A.ndim == 2 else A.shape
+        kn = None
+        if mask is not None:
+            kn = np.ascontiguousarray(mask)
+            if kn.dtype != np.uint8:
+                kn = (kn != 0).astype(np.uint8)
+            if kn.shape != A.shape:
+                raise ValueError("mse_missing: dimension mismatch")
+        out = (N.tf_quality_metrics * frames)()
+        check(lib().tf_quality(self._h, A.ctypes.data, B.ctypes.data,
+                               kn.ctypes.data if kn is not None else None, W, H, frames,
+                               int(bool(ssim)), out))
+        return [{f: getattr(q, f) for f, _ in N.tf_quality_metrics._fields_} for q in out]
+
+    def quality_device(self, d_a: int, d_b: int, d_known: int | None, W: int, H: int,
+                       frames: int = 1, ssim: bool = True, stream: int = 0, gpu: int = 0) -> list[dict]:
+        out = (N.tf_quality_metrics * frames)()
+        check(lib().tf_quality_device(self._h, gpu, d_a, d_b, d_known or None, W, H, frames,
+                                      int(bool(ssim)), stream or None, out))
+        return [{f: getattr(q, f) for f, _ in N.tf_quality_metrics._fields_} for q in out]
+
     # -- device path (inputs already in HBM; torch tensors or raw pointers)
     def tiled_device(self, d_img: int, d_known: int, d_out: int, W: int, H: int, frames: int,
                      tiles: int, overlap: int, params: FseLiteParams, stream: int = 0,
@@ -234,6 +264,58 @@ def default_context(device: int = 0, mode: str = "exact") -> Context:
         if key not in _default_ctx:
             _default_ctx[key] = Context(1, [device], mode)
         return _default_ctx[key]
+
+
+# ---------------------------------------------------------------- metrics (metrics.hpp)
+def _single(a: np.ndarray, b: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    A = np.ascontiguousarray(a, dtype=np.uint8)
+    B = np.ascontiguousarray(b, dtype=np.uint8)
+    if A.ndim != 2 or A.shape != B.shape:
+        raise ValueError("dimension mismatch")
+    return A, B
+
+
+def mse(a: np.ndarray, b: np.ndarray, device: int = 0) -> float:
+    """metrics.hpp:12-24 on the GPU (bit-identical)."""
+    A, B = _single(a, b)
+    v = C.c_double()
+    check(lib().tf_mse(default_context(device).handle, A.ctypes.data, B.ctypes.data, A.shape[1],
+                       A.shape[0], C.byref(v)))
+    return v.value
+
+
+def mse_missing(a: np.ndarray, b: np.ndarray, mask: np.ndarray, device: int = 0) -> float:
+    """metrics.hpp:27-45: MSE over the pixels the mask marks unknown (ValueError if none)."""
+    A, B = _single(a, b)
+    kn = np.ascontiguousarray((np.asarray(mask) != 0).astype(np.uint8))
+    if kn.shape != A.shape:
+        raise ValueError("mse_missing: dimension mismatch")
+    v = C.c_double()
+    check(lib().tf_mse_missing(default_context(device).handle, A.ctypes.data, B.ctypes.data,
+                               kn.ctypes.data, A.shape[1], A.shape[0], C.byref(v)))
+    return v.value
+
+
+def psnr_from_mse(mse_value: float) -> float:
+    return lib().tf_psnr_from_mse(float(mse_value))
+
+
+def psnr(a: np.ndarray, b: np.ndarray, device: int = 0) -> float:
+    """metrics.hpp:52-55 on the GPU (bit-identical); +inf for identical images."""
+    A, B = _single(a, b)
+    v = C.c_double()
+    check(lib().tf_psnr(default_context(device).handle, A.ctypes.data, B.ctypes.data, A.shape[1],
+                        A.shape[0], C.byref(v)))
+    return v.value
+
+
+def ssim(a: np.ndarray, b: np.ndarray, device: int = 0) -> float:
+    """metrics.hpp:58-88 on the GPU (window values bit-identical, mean within 1e-12 rel.)."""
+    A, B = _single(a, b)
+    v = C.c_double()
+    check(lib().tf_ssim(default_context(device).handle, A.ctypes.data, B.ctypes.data, A.shape[1],
+                        A.shape[0], C.byref(v)))
+    return v.value
 
 
 # ---------------------------------------------------------------- extrapolators
