@@ -142,9 +142,17 @@ struct WarpLayout {
 #endif
 constexpr int kHalfWB = (TF_HALF_W32 || TF_HALF_ACC32) ? 8 : 16;  // bytes per W element
 
+// Windows up to 16 x 16 (one warp, <= 5 rows per lane) keep the selection log in shared
+// memory (after the sync area) instead of a global scratch: short loops, where the per-
+// iteration log store and the post-loop copy back were a visible share (config 3).
+__host__ __device__ constexpr bool half_slog(int nt, int bpth, bool gen) {
+  return !gen && nt == 32 && bpth <= 5;
+}
+
 struct HalfLayout {
-  int wbytes, off_tw, off_sync, total;
-  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt) {
+  int wbytes, off_tw, off_sync, off_log, total;
+  // log_iters > 0: room for the selection log (double2 + int32 per iteration) at off_log
+  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt, int log_iters = 0) {
     const int lmax = bpth * (nt / M) - 1;
     const int rows = kHalfWB * M * (L + lmax + 1);
     int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
@@ -155,6 +163,8 @@ struct HalfLayout {
     off_tw = wbytes;
     off_sync = off_tw + 32 * wmax + 32 * wmax;  // FP64 twiddles x/y, FP32 x/y/y-swapped/x-swapped
     total = off_sync + 4 * 32 + 16;  // argmax slots (two warps), block id, sum of weights
+    off_log = (total + 15) & ~15;
+    if (log_iters > 0) total = off_log + 20 * log_iters;
   }
 };
 
