@@ -17,8 +17,9 @@ value  : device path, inputs resident in HBM (tf_tiled_extrapolate_device),
          headline mode (default FAST: FMA + Hermitian half spectrum, within the north-star
          tolerance, checked on this very frame and reported under "parity"); the EXACT
          mode (byte-identical to the reference, also checked here) is timed and reported.
-e2e    : the same through the C-ABI with pinned HOST buffers: H2D of image +
-         mask, FSE, gather, D2H of the result, all inside the timed region.
+e2e    : the same through the public host-buffer call (tf_tiled_extrapolate on pinned
+         HOST buffers): H2D of image + mask, FSE, D2H of the result inside the call
+         (streamed in row bands so copies overlap the kernels), every rank its own frame.
 roofline: FP64-bound kernels; achieved = executed FP64 flops per launch (== the
          SURVEY §8(d) algorithmic sum_b F_b in EXACT mode) / mean FSE time (CUDA events
          on the launch stream), peak = FP64 DFMA rate measured live (tf_calibrate).
@@ -233,7 +234,7 @@ def main():
     d_kn = h_kn.to(dev)
     d_out = torch.empty_like(d_img)
     d_all = torch.empty(world * fb, dtype=torch.uint8, device=dev) if (world > 1 and rank == 0) else None
-    h_res = torch.empty(world * fb if rank == 0 else fb, dtype=torch.uint8).pin_memory()
+    h_res = torch.empty(fb, dtype=torch.uint8).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     p = wl.params._c()
 
@@ -246,15 +247,11 @@ def main():
                                      d_all.data_ptr() if d_all is not None else None, fb, 0, sptr))
 
     def e2e_step():
-        with torch.cuda.stream(stream):
-            d_img.copy_(h_img, non_blocking=True)
-            d_kn.copy_(h_kn, non_blocking=True)
-        device_step()
-        with torch.cuda.stream(stream):
-            if rank == 0:
-                h_res.copy_(d_all if d_all is not None else d_out, non_blocking=True)
-            else:
-                h_res.copy_(d_out, non_blocking=True)
+        # the call a user makes: tf_tiled_extrapolate on pinned HOST buffers (the library
+        # streams row bands: H2D, FSE and D2H overlap inside the call); every rank
+        # reconstructs its own frame into its own host memory
+        N.check(L.tf_tiled_extrapolate(ctx.handle, h_img.data_ptr(), h_kn.data_ptr(), W, H, 1, wl.tiles,
+                                       wl.overlap, C.byref(p), h_res.data_ptr(), None))
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -362,7 +359,8 @@ def main():
                    "parallelism": f"dp{world} frames, NCCL gather to rank 0" if world > 1 else "single GPU",
                    "blocks_processed": st.blocks_processed, "blocks_reference": st.blocks_reference},
         "e2e": {"value": round(e2e, 3), "unit": "Mpixel/s", "ms_per_step": round(ms_e2e, 4),
-                "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": (world * fb if rank == 0 else fb)},
+                "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb,
+                "path": "tf_tiled_extrapolate (host buffers, streamed row bands), per rank"},
         "gpu_launches": args.steps * 3,  # enumerate + warp-per-block FSE + border-window FSE per step
         "roofline": roof,
         "clocks": res["clocks"],

@@ -130,6 +130,12 @@ struct Gpu {
   bool fft_ok = false;        // c_fft32 uploaded on this device
   int wide_occ[3][65] = {};    // FAST wide kernel occupancy per (precision variant, window side)
   int wide_smem[3][65] = {};
+  // streamed host path: copy-in / copy-out streams, a second compute stream, band events
+  static constexpr int kMaxBands = 16;
+  cudaStream_t cin = nullptr, cout = nullptr, stream2 = nullptr;
+  cudaStream_t bs[kMaxBands] = {}, bside[kMaxBands] = {};  // per-band compute / fork streams
+  cudaEvent_t ev_in[kMaxBands] = {}, ev_done[kMaxBands] = {};
+  int last_slots = 1;         // band slots used by the last host-path run (stats)
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
@@ -276,11 +282,26 @@ struct DevRun {
   double kernel_ms = 0.0, flops = 0.0, flops_executed = 0.0;
 };
 
+// Row band of the streamed host path (tf_tiled_extrapolate on one GPU): only blocks whose
+// first row (flattened over frames) lies in [row0, row1); slot selects the band's counters,
+// block lists and log scratch; the caller initialises d_out and brackets the timing events.
+struct Band {
+  int64_t row0 = 0, row1 = INT64_MAX;
+  int slot = 0, nslots = 1;
+  int64_t cand = 0;   // candidate blocks of the band (grid bound)
+  bool first = true;  // uploads the tile table and the constant tables
+};
+
 // Enqueue one GPU's share (tiles t % n_parts == part) of a tiled job.
 static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                       const uint8_t* d_known, int W, int H, int frames, const tf_fse_params& p,
                       int part, int n_parts, uint8_t* d_out, cudaStream_t s, bool want_stats,
-                      DevRun* res) {
+                      DevRun* res, const Band* band = nullptr) {
+  const Band whole;
+  const Band& bd = band ? *band : whole;
+  const size_t bslot = static_cast<size_t>(bd.slot), nslots = static_cast<size_t>(bd.nslots);
+  const int64_t cand = band ? bd.cand : pl.cand_blocks;
+  cudaStream_t side = band ? g.bside[bd.slot] : g.side;  // fork stream of the border kernels
   const bool exact = ctx->mode == TF_MODE_EXACT;
   // bins the CTA kernel's threads carry: the full window, or FAST's Hermitian half
   const bool half = tfb::cta_half(exact);
@@ -384,31 +405,37 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                  nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
                  wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0, wide,
                  wide_smem, wide ? g.wide_occ[w64][wide] : 0);
-  int rc = upload_tables(g, p, pl.wmax, s);
-  if (rc != TF_OK) return rc;
-
+  int rc = TF_OK;
   const size_t n_tiles = pl.tiles.size();
-  // table upload through pinned staging; wait for the previous upload first
-  if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
-  rc = ensure_pinned(g, n_tiles * sizeof(TileDesc));
-  if (rc != TF_OK) return rc;
-  std::memcpy(g.pinned, pl.tiles.data(), n_tiles * sizeof(TileDesc));
-  TF_CUDA(g.tiles.ensure(n_tiles * sizeof(TileDesc)));
-  TF_CUDA(g.blocks.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
-  TF_CUDA(g.wblocks.ensure(static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
-  TF_CUDA(g.counters.ensure(4 * sizeof(int32_t)));
-  TF_CUDA(g.refblk.ensure(n_tiles * sizeof(unsigned long long)));
-  TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
-  TF_CUDA(cudaEventRecord(g.ev_tables, s));
-  TF_CUDA(cudaMemsetAsync(g.counters.p, 0, 4 * sizeof(int32_t), s));
-  TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, n_tiles * sizeof(unsigned long long), s));
+  if (bd.first) {
+    rc = upload_tables(g, p, pl.wmax, s);
+    if (rc != TF_OK) return rc;
+    // table upload through pinned staging; wait for the previous upload first
+    if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
+    rc = ensure_pinned(g, n_tiles * sizeof(TileDesc));
+    if (rc != TF_OK) return rc;
+    std::memcpy(g.pinned, pl.tiles.data(), n_tiles * sizeof(TileDesc));
+    TF_CUDA(g.tiles.ensure(n_tiles * sizeof(TileDesc)));
+    TF_CUDA(g.blocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+    TF_CUDA(g.wblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+    TF_CUDA(g.counters.ensure(nslots * 4 * sizeof(int32_t)));
+    TF_CUDA(g.refblk.ensure(nslots * n_tiles * sizeof(unsigned long long)));
+    TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
+    TF_CUDA(cudaMemsetAsync(g.counters.p, 0, nslots * 4 * sizeof(int32_t), s));
+    TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, nslots * n_tiles * sizeof(unsigned long long), s));
+    // later bands (other streams) wait on this: tile table and every slot's counters ready
+    TF_CUDA(cudaEventRecord(g.ev_tables, s));
+  }
+  int32_t* counters = g.counters.as<int32_t>() + 4 * bslot;
+  BlockDesc* blocks = g.blocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
+  BlockDesc* wblocks = g.wblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   if (want_stats) {
     // [CTA-kernel blocks | warp-kernel blocks]
     TF_CUDA(g.stats.ensure(2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
     TF_CUDA(cudaMemsetAsync(g.stats.p, 0, 2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
   }
   const size_t frame_bytes = static_cast<size_t>(W) * H * frames;
-  if (d_out != d_img)
+  if (d_out != d_img && !band)
     TF_CUDA(cudaMemcpyAsync(d_out, d_img, frame_bytes, cudaMemcpyDeviceToDevice, s));
 
   tfb::EnumLaunch e{};
@@ -420,14 +447,16 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   e.n_tiles = static_cast<int32_t>(n_tiles);
   e.part = part;
   e.n_parts = n_parts;
-  e.blocks = g.blocks.as<BlockDesc>();
-  e.n_blocks = g.counters.as<int32_t>();
-  e.ref_blocks = g.refblk.as<unsigned long long>();
+  e.blocks = blocks;
+  e.n_blocks = counters;
+  e.ref_blocks = g.refblk.as<unsigned long long>() + bslot * n_tiles;
+  e.row0 = bd.row0;
+  e.row1 = bd.row1;
   e.margin = p.margin;
   e.warp_M = (wbpt || wide) ? span : 0;
   e.warp_L = (wbpt || wide) ? span : 0;
-  e.wblocks = g.wblocks.as<BlockDesc>();
-  e.n_wblocks = g.counters.as<int32_t>() + 2;
+  e.wblocks = wblocks;
+  e.n_wblocks = counters + 2;
   TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
 
   tfb::FseLaunch a{};
@@ -437,9 +466,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   a.W = W;
   a.H = H;
   a.tiles = g.tiles.as<TileDesc>();
-  a.blocks = g.blocks.as<BlockDesc>();
-  a.n_blocks = g.counters.as<int32_t>();
-  a.next_block = g.counters.as<int32_t>() + 1;
+  a.blocks = blocks;
+  a.n_blocks = counters;
+  a.next_block = counters + 1;
   a.B = p.block;
   a.margin = p.margin;
   a.iters = p.iters;
@@ -449,61 +478,68 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   a.wmax = pl.wmax;
   a.stats = want_stats ? g.stats.as<BlockStat>() : nullptr;
   int grid = g.sms * g.occ[exact][cfg];
-  if (pl.cand_blocks < grid) grid = static_cast<int>(std::max<int64_t>(1, pl.cand_blocks));
+  if (cand < grid) grid = static_cast<int>(std::max<int64_t>(1, cand));
   const int slot = static_cast<int>(g.launches % Gpu::kRing);
   if (!g.ring0[slot]) {
     TF_CUDA(cudaEventCreate(&g.ring0[slot]));
     TF_CUDA(cudaEventCreate(&g.ring1[slot]));
   }
-  TF_CUDA(cudaEventRecord(g.ev0, s));
-  TF_CUDA(cudaEventRecord(g.ring0[slot], s));
+  if (!band) {
+    TF_CUDA(cudaEventRecord(g.ev0, s));
+    TF_CUDA(cudaEventRecord(g.ring0[slot], s));
+  }
   const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
   if (wide) {
     // border windows (CTA kernel) on a forked stream, concurrently with the wide kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
-    TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
-    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
-    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
+    TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
+    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+    TF_CUDA(cudaEventRecord(g.ev_join, side));
     const int wgrid = g.sms * g.wide_occ[w64][wide];
-    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(int32_t)));
-    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid) * p.iters * sizeof(double2)));
+    const size_t per = static_cast<size_t>(wgrid) * p.iters;  // log entries per band slot
+    TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
+    TF_CUDA(g.wlog_c.ensure(nslots * per * sizeof(double2)));
     tfb::FseLaunch w = a;
-    w.blocks = g.wblocks.as<BlockDesc>();
-    w.n_blocks = g.counters.as<int32_t>() + 2;
-    w.next_block = g.counters.as<int32_t>() + 3;
+    w.blocks = wblocks;
+    w.n_blocks = counters + 2;
+    w.next_block = counters + 3;
     w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
-    w.wlog_kl = g.wlog_kl.as<int32_t>();
-    w.wlog_c = g.wlog_c.as<double2>();
-    TF_CUDA(tfb::fse_wide_launch(wide, w64, w, wgrid, wide_smem, s));
+    w.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per;
+    w.wlog_c = g.wlog_c.as<double2>() + bslot * per;
+    TF_CUDA(tfb::fse_wide_launch(wide, w64, w,
+                                 static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1))),
+                                 wide_smem, s));
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else if (wbpt) {
     // border windows (CTA kernel) on a forked stream, concurrently with the warp kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
-    TF_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
+    TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
     const int wgrid = g.sms * g.wocc[exact][wbpt];
     const int ggrid = gbpth ? std::min(g.sms * g.gocc[gbpth], std::max(grid, 1)) : 0;
-    TF_CUDA(g.wlog_kl.ensure(static_cast<size_t>(wgrid + ggrid) * p.iters * sizeof(int32_t)));
-    TF_CUDA(g.wlog_c.ensure(static_cast<size_t>(wgrid + ggrid) * p.iters * sizeof(double2)));
+    const size_t per = static_cast<size_t>(wgrid + ggrid) * p.iters;  // log entries per band slot
+    TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
+    TF_CUDA(g.wlog_c.ensure(nslots * per * sizeof(double2)));
     if (gbpth) {
       tfb::FseLaunch ga = a;
-      ga.wlog_kl = g.wlog_kl.as<int32_t>() + static_cast<size_t>(wgrid) * p.iters;
-      ga.wlog_c = g.wlog_c.as<double2>() + static_cast<size_t>(wgrid) * p.iters;
-      TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, g.side));
+      ga.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
+      ga.wlog_c = g.wlog_c.as<double2>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
+      TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, side));
     } else {
-      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, g.side));
+      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
     }
-    TF_CUDA(cudaEventRecord(g.ev_join, g.side));
+    TF_CUDA(cudaEventRecord(g.ev_join, side));
     tfb::FseLaunch w = a;
-    w.blocks = g.wblocks.as<BlockDesc>();
-    w.n_blocks = g.counters.as<int32_t>() + 2;
-    w.next_block = g.counters.as<int32_t>() + 3;
+    w.blocks = wblocks;
+    w.n_blocks = counters + 2;
+    w.next_block = counters + 3;
     w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
-    w.wlog_kl = g.wlog_kl.as<int32_t>();
-    w.wlog_c = g.wlog_c.as<double2>();
+    w.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per;
+    w.wlog_c = g.wlog_c.as<double2>() + bslot * per;
+    const int wg = static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1)));
     if (wkind == 1)
-      TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wgrid, wsmem, s));
+      TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wg, wsmem, s));
     else
-      TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wgrid, wsmem, s));
+      TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wg, wsmem, s));
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
@@ -514,9 +550,11 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "[tframe] warp blocks %d, cta blocks %d\n", cnt[2], cnt[0]);
   }
-  TF_CUDA(cudaEventRecord(g.ring1[slot], s));
-  TF_CUDA(cudaEventRecord(g.ev1, s));
-  ++g.launches;
+  if (!band) {
+    TF_CUDA(cudaEventRecord(g.ring1[slot], s));
+    TF_CUDA(cudaEventRecord(g.ev1, s));
+    ++g.launches;
+  }
 
   if (want_stats && res) {
     TF_CUDA(cudaStreamSynchronize(s));
@@ -703,6 +741,21 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.ev_fork) cudaEventDestroy(g.ev_fork);
     if (g.ev_join) cudaEventDestroy(g.ev_join);
     if (g.side) cudaStreamDestroy(g.side);
+    for (cudaStream_t* st : {&g.cin, &g.cout, &g.stream2})
+      if (*st) {
+        cudaStreamSynchronize(*st);
+        cudaStreamDestroy(*st);
+      }
+    for (int k = 0; k < Gpu::kMaxBands; ++k)
+      for (cudaStream_t st : {g.bs[k], g.bside[k]})
+        if (st) {
+          cudaStreamSynchronize(st);
+          cudaStreamDestroy(st);
+        }
+    for (int k = 0; k < Gpu::kMaxBands; ++k) {
+      if (g.ev_in[k]) cudaEventDestroy(g.ev_in[k]);
+      if (g.ev_done[k]) cudaEventDestroy(g.ev_done[k]);
+    }
     if (g.stream) cudaStreamDestroy(g.stream);
   }
   if (ctx->rank_comm && nccl().ok) nccl().CommDestroy(ctx->rank_comm);
@@ -759,6 +812,102 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
 
 // Gather the cores of GPUs 1..n-1 into GPU 0 (NCCL send/recv over NVLink), download the
 // merged frames from GPU 0 and wait for every GPU (run_master's merge, runtime.hpp:112-130).
+// Streamed host path on one GPU (tf_tiled_extrapolate with host buffers): the frames are cut
+// into nb row bands (rows flattened over frames).  Copy-in stream: band k's image and mask
+// rows H2D, then the output rows initialised from the image (D2D).  Compute (two
+// per-band streams): band k's blocks (first row in band k) once every band its windows
+// reach has arrived.  Copy-out stream: band k's output rows D2H once bands k-1 and k are
+// computed (a block writes only its own B <= R rows).  The H2D of later bands and the D2H
+// of earlier ones overlap the FSE kernels; outputs are identical to the one-shot path.
+static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
+                        const uint8_t* known, int W, int H, int frames, const tf_fse_params& p,
+                        uint8_t* out, int nb) {
+  const auto t_start = clk::now();
+  const int64_t rows = static_cast<int64_t>(frames) * H;
+  const int64_t R = (rows + nb - 1) / nb;
+  for (cudaStream_t* st : {&g.cin, &g.cout, &g.stream2})
+    if (!*st) TF_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+  for (int k = 0; k < Gpu::kMaxBands; ++k) {
+    if (!g.ev_in[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_in[k], cudaEventDisableTiming));
+    if (!g.ev_done[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_done[k], cudaEventDisableTiming));
+    if (!g.bs[k]) TF_CUDA(cudaStreamCreateWithFlags(&g.bs[k], cudaStreamNonBlocking));
+    if (!g.bside[k]) TF_CUDA(cudaStreamCreateWithFlags(&g.bside[k], cudaStreamNonBlocking));
+  }
+  const size_t bytes = static_cast<size_t>(W) * rows;
+  TF_CUDA(g.img.ensure(bytes));
+  TF_CUDA(g.known.ensure(bytes));
+  TF_CUDA(g.out.ensure(bytes));
+  uint8_t* di = g.img.as<uint8_t>();
+  uint8_t* dk = g.known.as<uint8_t>();
+  uint8_t* dout = g.out.as<uint8_t>();
+  // the previous call's copy-out must be done with g.out before it is overwritten
+  TF_CUDA(cudaStreamSynchronize(g.cout));
+  // copy-in in finer chunks than the compute bands: a band waits only for the chunk that
+  // holds the last row its windows reach
+  const int nin = std::min(Gpu::kMaxBands, std::max(nb, 8));
+  const int64_t Rin = (rows + nin - 1) / nin;
+  for (int k = 0; k < nin; ++k) {
+    const int64_t r0 = k * Rin, r1 = std::min(rows, r0 + Rin);
+    if (r1 > r0) {
+      const size_t off = static_cast<size_t>(r0) * W, n = static_cast<size_t>(r1 - r0) * W;
+      TF_CUDA(cudaMemcpyAsync(di + off, img + off, n, cudaMemcpyHostToDevice, g.cin));
+      TF_CUDA(cudaMemcpyAsync(dk + off, known + off, n, cudaMemcpyHostToDevice, g.cin));
+      TF_CUDA(cudaMemcpyAsync(dout + off, di + off, n, cudaMemcpyDeviceToDevice, g.cin));
+    }
+    TF_CUDA(cudaEventRecord(g.ev_in[k], g.cin));
+  }
+  const int span = p.block + p.margin;  // rows a window reaches below its block's first row
+  for (int k = 0; k < nb; ++k) {
+    Band b;
+    b.row0 = k * R;
+    b.row1 = std::min(rows, b.row0 + R);
+    b.slot = k;
+    b.nslots = nb;
+    b.first = k == 0;
+    for (const TileDesc& t : pl.tiles) {  // candidate blocks with their first row in the band
+      const int64_t f0 = static_cast<int64_t>(t.frame) * H + t.hy;
+      const int64_t lo = std::max<int64_t>(0, (b.row0 - f0 + p.block - 1) / p.block);
+      const int64_t hi = std::min<int64_t>(t.gh, b.row1 - f0 <= 0 ? 0 : (b.row1 - f0 + p.block - 1) / p.block);
+      if (hi > lo) b.cand += (hi - lo) * t.gw;
+    }
+    // one stream per band: every band's kernels can run as soon as its rows have arrived,
+    // the CTAs of earlier-launched bands are dispatched first
+    cudaStream_t cs = g.bs[k];
+    // last row the band's windows reach, and the first row of the next band (whose
+    // output rows this band's blocks may write: they must be initialised first)
+    const int64_t maxrow = std::min(rows - 1, std::max(b.row1 - 1 + span, b.row1));
+    const int need = static_cast<int>(std::min<int64_t>(nin - 1, maxrow / Rin));
+    TF_CUDA(cudaStreamWaitEvent(cs, g.ev_in[need], 0));
+    if (k == 0) TF_CUDA(cudaEventRecord(g.ev0, cs));
+    if (k > 0) TF_CUDA(cudaStreamWaitEvent(cs, g.ev_tables, 0));  // tile table + counters
+    const int rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b);
+    if (rc != TF_OK) return rc;
+    TF_CUDA(cudaEventRecord(g.ev_done[k], cs));
+  }
+  for (int k = 0; k < nb; ++k) {
+    const int64_t r0 = k * R, r1 = std::min(rows, r0 + R);
+    TF_CUDA(cudaStreamWaitEvent(g.cout, g.ev_done[k], 0));
+    if (k > 0) TF_CUDA(cudaStreamWaitEvent(g.cout, g.ev_done[k - 1], 0));
+    if (r1 <= r0) continue;
+    const size_t off = static_cast<size_t>(r0) * W, n = static_cast<size_t>(r1 - r0) * W;
+    TF_CUDA(cudaMemcpyAsync(out + off, dout + off, n, cudaMemcpyDeviceToHost, g.cout));
+  }
+  for (int k = 0; k < nb; ++k) TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_done[k], 0));
+  TF_CUDA(cudaEventRecord(g.ev1, g.stream));
+  g.last_slots = nb;
+  const auto t_enq = clk::now();
+  TF_CUDA(cudaStreamSynchronize(g.cout));
+  TF_CUDA(cudaStreamSynchronize(g.stream));
+  if (std::getenv("TF_STREAM_DEBUG")) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g.ev0, g.ev1);
+    std::fprintf(stderr, "[tframe] streamed %d bands: enqueue %lld us, total %lld us, compute span %.1f us\n",
+                 nb, static_cast<long long>(std::chrono::duration_cast<std::chrono::microseconds>(t_enq - t_start).count()),
+                 static_cast<long long>(us_since(t_start)), ms * 1e3);
+  }
+  return TF_OK;
+}
+
 static int gather_download(tf_ctx* ctx, const Plan& pl, int W, int H, size_t bytes, uint8_t* out) {
   const int n = static_cast<int>(ctx->gpus.size());
   int rc = TF_OK;
@@ -838,6 +987,46 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
   const int64_t plan_us = us_since(t0);
   const int n = static_cast<int>(ctx->gpus.size());
   const size_t bytes = static_cast<size_t>(W) * H * frames;
+  // ---- one GPU: streamed row bands (copy-in / compute / copy-out overlap), unless the
+  // frames are too short to split (TF_STREAM_BANDS overrides the band count, 1 = one shot)
+  int nbands = 1;
+  if (n == 1) {
+    const int64_t rows = static_cast<int64_t>(frames) * H;
+    // measured per call (host API, pinned buffers; one-shot / best): c2 0.862 / 0.835 ms at
+    // 4 bands, c3 6.93 / 6.75 ms at 4-8, c4 15.24 / 14.17 ms at 8; the host enqueue costs
+    // ~25-35 us per band and banding adds ~5 % compute (smaller launches), so bands stay a
+    // few hundred rows tall
+    nbands = static_cast<int>(std::clamp<int64_t>(rows / 256, 1, 8));
+    if (const char* e = std::getenv("TF_STREAM_BANDS")) nbands = std::atoi(e);
+    nbands = std::max(1, std::min(nbands, Gpu::kMaxBands));
+    if ((rows + nbands - 1) / nbands < p->block) nbands = 1;  // a block spans at most 2 bands
+  }
+  if (nbands > 1) {
+    Gpu& g = ctx->gpus[0];
+    rc = select_device(g);
+    if (rc != TF_OK) return rc;
+    const auto t_d = clk::now();
+    rc = run_streamed(ctx, g, pl, img, known, W, H, frames, *p, out, nbands);
+    if (rc != TF_OK) return rc;
+    if (stats) {
+      *stats = tf_run_stats{};
+      stats->plan_us = plan_us;
+      stats->compute_span_us = us_since(t_d);
+      stats->total_us = us_since(t0);
+      stats->overhead_pixels = pl.overhead;
+      float ms = 0.f;
+      TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+      stats->kernel_ms = ms;
+      std::vector<int32_t> cnt(4 * static_cast<size_t>(nbands));
+      TF_CUDA(cudaMemcpy(cnt.data(), g.counters.p, cnt.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      std::vector<unsigned long long> ref(pl.tiles.size() * static_cast<size_t>(nbands));
+      TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+      for (int k = 0; k < nbands; ++k) stats->blocks_processed += cnt[4 * k] + cnt[4 * k + 2];
+      for (unsigned long long r : ref) stats->blocks_reference += static_cast<int64_t>(r);
+    }
+    return TF_OK;
+  }
   // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
   std::vector<DevRun> dr(static_cast<size_t>(n));
   for (int gi = 0; gi < n; ++gi) {

@@ -66,6 +66,9 @@ struct EnumLaunch {
   int32_t warp_M, warp_L;     // windows of exactly this size go to the warp kernel (0 = none)
   BlockDesc* wblocks;         // out: blocks for the warp kernel
   int32_t* n_wblocks;
+  // row band (streamed host path): only blocks whose first row, flattened over frames
+  // (frame * H + halo y + block y), lies in [row0, row1) are counted and enqueued
+  int64_t row0, row1;
 };
 
 constexpr int kCY = 4;  // rows per DFT chunk

@@ -255,3 +255,25 @@ def test_exact_mode_full_config_frame_equals_reference(ctx, cfg):
                                 p.model_iterations, p.compensation, p.weight_decay)
     got, _ = ctx.tiled(img, kn, wl.tiles, wl.overlap, p)
     assert int((got != want).sum()) == 0
+
+
+@pytest.mark.parametrize("cfg,frames", [(2, 1), (3, 1), (5, 3), (1, 1)])
+def test_streamed_host_path_equals_one_shot(ctx, fctx, cfg, frames, monkeypatch):
+    """The single-GPU host path streams row bands (H2D / FSE / D2H overlap over streams); its
+    output and block counts must equal the one-shot path (TF_STREAM_BANDS=1) for any band
+    count, in both modes, including multi-frame batches."""
+    from paper_2207_00238_b200.configs import workload
+    wl = workload(cfg, frames=frames)
+    W, H = (wl.W, wl.H) if cfg != 3 else (960, 540)
+    imgs, kns = zip(*[T.synth_frame(cfg, f, W, H) for f in range(frames)])
+    img = np.stack(imgs) if frames > 1 else imgs[0]
+    kn = np.stack(kns) if frames > 1 else kns[0]
+    for c in (ctx, fctx):
+        monkeypatch.setenv("TF_STREAM_BANDS", "1")
+        want, st1 = c.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+        for nb in ("2", "5", "8", "16"):
+            monkeypatch.setenv("TF_STREAM_BANDS", nb)
+            got, st = c.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+            assert np.array_equal(got, want), f"c{cfg} {c.mode} bands={nb}: {(got != want).sum()} pixels differ"
+            assert st.blocks_processed == st1.blocks_processed
+            assert st.blocks_reference == st1.blocks_reference
