@@ -44,3 +44,52 @@ def test_reference_master_with_gpu_diffusion_workers():
     assert r.returncode == 0, r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["bytes_equal"], out
+
+
+TCP_EXE = ROOT / "integration" / "_build" / "ref_tcp_gpu_workers"
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workers,cfg,W,H", [(2, 2, 480, 270), (3, 3, 320, 180)])
+def test_reference_tcp_master_with_gpu_workers_in_process(workers, cfg, W, H):
+    """The reference's TcpMasterTransport + TcpWorkerEndpoint (TFRM frames over loopback
+    sockets) with GPU worker loops: byte-identical to the stock CPU workers."""
+    if not TCP_EXE.exists():
+        pytest.skip("integration binary not built")
+    r = subprocess.run([str(TCP_EXE), "selftest", str(_free_port()), str(workers), str(cfg), str(W), str(H),
+                        "exact"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["bytes_equal"], out
+
+
+@pytest.mark.gpu
+def test_reference_tcp_master_with_gpu_worker_processes():
+    """Separate worker processes (one per GPU / box in a deployment) connecting to the
+    reference's master over TCP."""
+    if not TCP_EXE.exists():
+        pytest.skip("integration binary not built")
+    port = _free_port()
+    master = subprocess.Popen([str(TCP_EXE), "master", str(port), "2", "2", "480", "270", "exact"],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+    workers = [subprocess.Popen([str(TCP_EXE), "worker", f"127.0.0.1:{port}", "0", "exact"],
+                                stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for _ in range(2)]
+    try:
+        out, err = master.communicate(timeout=120)
+        for w in workers:
+            w.wait(timeout=60)
+    finally:
+        for p in [master, *workers]:
+            if p.poll() is None:
+                p.kill()
+    assert master.returncode == 0, err
+    assert all(w.returncode == 0 for w in workers), [w.stderr.read() for w in workers]
+    res = json.loads(out.strip().splitlines()[-1])
+    assert res["bytes_equal"] and res["transport"] == "tcp", res
