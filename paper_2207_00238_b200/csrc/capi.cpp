@@ -128,6 +128,7 @@ struct Gpu {
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
   bool fft_ok = false;        // c_fft32 uploaded on this device
+  int pair_occ = 0, pair_smem = 0;  // FAST pair kernel (16x16 windows)
   int wide_occ[3][65] = {};    // FAST wide kernel occupancy per (precision variant, window side)
   int wide_smem[3][65] = {};
   // streamed host path: copy-in / copy-out streams, a second compute stream, band events
@@ -398,6 +399,24 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     if (gbpth && g.gocc[gbpth] < 1) gbpth = 0;
   }
   const int gsmem = gbpth ? tfb::HalfLayout(32, span, gbpth, std::max(pl.wmax, 32), 32).total : 0;
+  // FAST 16x16 full windows: the pair kernel (two blocks per warp; TF_NO_PAIR=1 keeps the
+  // one-block-per-warp half kernel)
+  int pair = 0, pair_smem = 0;
+  if (wkind == 2 && hnt == 32 && tfb::pair_supported(span)) {
+    const tfb::PairLayout prl(span, p.iters);
+    if (prl.total <= 227 * 1024) {
+      if (g.pair_smem != prl.total) {
+        int occ = 0;
+        TF_CUDA(tfb::fse_pair_prepare(span, prl.total, &occ));
+        g.pair_occ = occ;
+        g.pair_smem = prl.total;
+      }
+      if (g.pair_occ >= 1) {
+        pair = span;
+        pair_smem = prl.total;
+      }
+    }
+  }
   if (std::getenv("TF_VERBOSE"))
     std::fprintf(stderr,
                  "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d"
@@ -536,10 +555,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     w.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per;
     w.wlog_c = g.wlog_c.as<double2>() + bslot * per;
     const int wg = static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1)));
-    if (wkind == 1)
+    if (pair) {
+      const int pg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.pair_occ,
+                                                        std::max<int64_t>((cand + 1) / 2, 1)));
+      TF_CUDA(tfb::fse_pair_launch(pair, w, pg, pair_smem, s));
+    } else if (wkind == 1) {
       TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wg, wsmem, s));
-    else
+    } else {
       TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wg, wsmem, s));
+    }
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
@@ -593,7 +617,12 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                        8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
       fl += f;
       const bool warp_list = q >= static_cast<size_t>(cnt[0]);
-      if (wide && warp_list) {
+      if (pair && warp_list) {
+        // pair kernel: 9 half rows x 16 columns per block, DFT as the T2 scheme
+        const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
+        xfl += 8.0 * b.M * b.L * (b.L / 2 + 1) + 16.0 * Nh * b.M +
+               Nh * (11.0 * b.iters + 8.0 * b.pairs) + 11.0 * b.evaluated * b.iters;
+      } else if (wide && warp_list) {
         // wide kernel: pass 1 over y on the half rows (8 S^2 HR), pass 2 over x (16 Nh S),
         // loop and evaluation as the half kernel
         const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;

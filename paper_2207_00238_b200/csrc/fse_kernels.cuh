@@ -205,6 +205,26 @@ struct WideLayout {
   }
 };
 
+// FAST pair kernel (full 16 x 16 windows, config 3): two blocks per warp, one per half-warp
+// (lane -> column k, all 9 half-spectrum rows per lane).  Per half:
+//   [region: W FP32 rows 0..S+HR-1 | staging (w FP32, w*v FP64) | C(x, l)] then, after both
+//   halves, [selection logs: 2 x (double2 + int32) x iters][twiddles][misc]
+struct PairLayout {
+  int region, off_log, log_stride, off_tw, total;
+  __host__ __device__ PairLayout(int S, int iters) {
+    const int hr = S / 2 + 1;
+    int r = 8 * S * (S + hr);
+    const int stage = 12 * S * S, cx = 24 * hr * S;
+    r = r > stage ? r : stage;
+    r = r > cx ? r : cx;
+    region = (r + 15) & ~15;
+    off_log = 2 * region;
+    log_stride = (20 * iters + 15) & ~15;  // per half: double2 x iters, then int32 x iters
+    off_tw = off_log + 2 * log_stride;
+    total = off_tw + 32 * S + 16;
+  }
+};
+
 // ---- launch helpers (fse_kernels.cu)
 struct KernelCfg {
   int nt, bpt;
@@ -249,6 +269,10 @@ int64_t ssim_partials(int w, int h, int frames);
 cudaError_t quality_launch(const uint8_t* a, const uint8_t* b, const uint8_t* known, int w, int h,
                            int frames, int sms, unsigned long long* sse3, double* partial,
                            double* ssim_sum, cudaStream_t s);
+// FAST pair kernel (S = 16 only; 0 if unsupported)
+int pair_supported(int S);
+cudaError_t fse_pair_prepare(int S, int smem_bytes, int* warps_per_sm);
+cudaError_t fse_pair_launch(int S, const FseLaunch& a, int grid, int smem_bytes, cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,

@@ -1,6 +1,8 @@
 """Quick timing probe: FSE kernel time for a BASELINE config through the C-ABI."""
 import sys, time
 sys.path.insert(0, '.')
+import os
+os.environ.setdefault('TF_STREAM_BANDS', '1')  # one-shot host path: kernel_ms = the FSE launch itself
 import numpy as np
 from paper_2207_00238_b200 import tframe as T
 from paper_2207_00238_b200.configs import CONFIGS

@@ -2,6 +2,8 @@
 against EXACT on full BASELINE frames (configs 1, 4, 5)."""
 import os, sys
 sys.path.insert(0, '.')
+import os
+os.environ.setdefault('TF_STREAM_BANDS', '1')  # one-shot host path: kernel_ms = the FSE launch itself
 import numpy as np
 from paper_2207_00238_b200 import tframe as T
 from paper_2207_00238_b200.configs import workload
