@@ -180,8 +180,11 @@ struct HalfLayout {
 //   [twiddles: FP64 (cos, sin) x S, FP32 (cos, -sin) x S, FP32 (sin, cos) x S][slots][misc]
 struct WideLayout {
   int nt, g, hr, bp, rows, region, off_tw, off_slots, off_misc, total;
+#ifndef TF_WIDE_NT1
+#define TF_WIDE_NT1 96  // threads per block of the FP64-DFT (WM1) variant for S <= 48 (192: c4 13.3 vs 12.1 ms)
+#endif
   __host__ __device__ static constexpr int threads(int S, int wm) {
-    return wm ? (S <= 48 ? 192 : 256) : (S <= 48 ? 96 : 128);
+    return wm == 2 ? (S <= 48 ? 192 : 256) : wm == 1 ? (S <= 48 ? TF_WIDE_NT1 : 256) : (S <= 48 ? 96 : 128);
   }
   __host__ __device__ WideLayout(int S, int iters, int wm) {
     nt = threads(S, wm);
