@@ -307,7 +307,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // bins the CTA kernel's threads carry: the full window, or FAST's Hermitian half
   const bool half = tfb::cta_half(exact);
   const int ncarry = half ? (pl.wmax / 2 + 1) * pl.wmax : pl.nmax;
-  const int cfg = tfb::pick_config(ncarry);
+  const int cfg = tfb::pick_config(ncarry, exact);
   if (cfg < 0)
     return set_error(TF_EUNSUPPORTED, "support window of " + std::to_string(pl.nmax) +
                                           " bins exceeds the kernel capacity (8192)");

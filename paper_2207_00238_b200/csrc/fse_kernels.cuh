@@ -234,7 +234,7 @@ struct KernelCfg {
 };
 constexpr int kNumCfgs = 10;
 extern const KernelCfg kCfgs[kNumCfgs];
-int pick_config(int nmax);  // smallest config holding nmax bins, -1 if none
+int pick_config(int nmax, bool exact);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
 cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                        cudaStream_t s);
