@@ -873,18 +873,24 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   TF_CUDA(cudaStreamSynchronize(g.cout));
   // copy-in in finer chunks than the compute bands: a band waits only for the chunk that
   // holds the last row its windows reach
+  // holds the last row its windows reach.  Chunks are enqueued just ahead of the first band
+  // that needs them, so band 0's kernels are enqueued after only its own chunks.
   const int nin = std::min(Gpu::kMaxBands, std::max(nb, 8));
   const int64_t Rin = (rows + nin - 1) / nin;
-  for (int k = 0; k < nin; ++k) {
-    const int64_t r0 = k * Rin, r1 = std::min(rows, r0 + Rin);
-    if (r1 > r0) {
-      const size_t off = static_cast<size_t>(r0) * W, n = static_cast<size_t>(r1 - r0) * W;
-      TF_CUDA(cudaMemcpyAsync(di + off, img + off, n, cudaMemcpyHostToDevice, g.cin));
-      TF_CUDA(cudaMemcpyAsync(dk + off, known + off, n, cudaMemcpyHostToDevice, g.cin));
-      TF_CUDA(cudaMemcpyAsync(dout + off, di + off, n, cudaMemcpyDeviceToDevice, g.cin));
+  int next_in = 0;
+  const auto copy_in_upto = [&](int last) -> int {
+    for (; next_in <= last; ++next_in) {
+      const int64_t r0 = next_in * Rin, r1 = std::min(rows, r0 + Rin);
+      if (r1 > r0) {
+        const size_t off = static_cast<size_t>(r0) * W, n = static_cast<size_t>(r1 - r0) * W;
+        TF_CUDA(cudaMemcpyAsync(di + off, img + off, n, cudaMemcpyHostToDevice, g.cin));
+        TF_CUDA(cudaMemcpyAsync(dk + off, known + off, n, cudaMemcpyHostToDevice, g.cin));
+        TF_CUDA(cudaMemcpyAsync(dout + off, di + off, n, cudaMemcpyDeviceToDevice, g.cin));
+      }
+      TF_CUDA(cudaEventRecord(g.ev_in[next_in], g.cin));
     }
-    TF_CUDA(cudaEventRecord(g.ev_in[k], g.cin));
-  }
+    return TF_OK;
+  };
   const int span = p.block + p.margin;  // rows a window reaches below its block's first row
   for (int k = 0; k < nb; ++k) {
     Band b;
@@ -906,12 +912,18 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     // output rows this band's blocks may write: they must be initialised first)
     const int64_t maxrow = std::min(rows - 1, std::max(b.row1 - 1 + span, b.row1));
     const int need = static_cast<int>(std::min<int64_t>(nin - 1, maxrow / Rin));
+    int rc = copy_in_upto(need);
+    if (rc != TF_OK) return rc;
     TF_CUDA(cudaStreamWaitEvent(cs, g.ev_in[need], 0));
     if (k == 0) TF_CUDA(cudaEventRecord(g.ev0, cs));
     if (k > 0) TF_CUDA(cudaStreamWaitEvent(cs, g.ev_tables, 0));  // tile table + counters
-    const int rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b);
+    rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b);
     if (rc != TF_OK) return rc;
     TF_CUDA(cudaEventRecord(g.ev_done[k], cs));
+  }
+  {
+    const int rc = copy_in_upto(nin - 1);  // (all chunks are needed by the last band already)
+    if (rc != TF_OK) return rc;
   }
   for (int k = 0; k < nb; ++k) {
     const int64_t r0 = k * R, r1 = std::min(rows, r0 + R);
