@@ -277,3 +277,32 @@ def test_streamed_host_path_equals_one_shot(ctx, fctx, cfg, frames, monkeypatch)
             assert np.array_equal(got, want), f"c{cfg} {c.mode} bands={nb}: {(got != want).sum()} pixels differ"
             assert st.blocks_processed == st1.blocks_processed
             assert st.blocks_reference == st1.blocks_reference
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_fast_kernels_with_empty_windows_and_odd_block_counts(ctx, fctx, cfg):
+    """FAST half / pair / wide kernels next to large holes: windows without a known pixel
+    give 128 (extrapolate.hpp:320-333), a half-warp whose block stops while its partner runs
+    (pair kernel) and odd block counts (idle half) behave; KAT: all-unknown frame -> 128."""
+    wl = CONFIGS[cfg]
+    p = wl.params
+    span = p.block_size + 2 * p.support_margin
+    W, H = 4 * span + 7, 3 * span + 5
+    img, kn = T.synth_frame(cfg, 1, W, H)
+    kn = kn.copy()
+    kn[span // 2: span // 2 + 2 * span, span: span + 2 * span] = 0  # hole wider than a window
+    for tiles in (1, 2, 3):
+        ex, st_e = ctx.tiled(img, kn, tiles, wl.overlap, p)
+        fa, st_f = fctx.tiled(img, kn, tiles, wl.overlap, p)
+        assert st_e.blocks_processed == st_f.blocks_processed
+        unk = kn == 0
+        assert np.array_equal(fa[~unk], img[~unk])
+        want = O.tiled(img, kn, tiles, wl.overlap, p.block_size, p.support_margin, p.model_iterations,
+                       p.compensation, p.weight_decay)[0]
+        assert np.array_equal(ex, want)
+        d = np.abs(ex.astype(int) - fa.astype(int))[unk]
+        assert (d <= 1).mean() >= FAST_WITHIN1, f"tiles={tiles}: max|d|={d.max()}"
+        assert np.array_equal(ex == 128, fa == 128) or (d <= 1).mean() >= FAST_WITHIN1
+    z = np.zeros_like(kn)
+    fa, _ = fctx.tiled(img, z, 2, wl.overlap, p)
+    assert (fa == 128).all()
