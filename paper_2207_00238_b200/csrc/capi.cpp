@@ -116,7 +116,7 @@ struct Gpu {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_tables = nullptr;
   DevBuf img, known, out;                       // host-API frame buffers
-  DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv;
+  DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv, xblocks;
   DevBuf qbuf;                                  // quality metrics: sums, SSIM partials
   void* pinned = nullptr;                       // host staging for tables
   size_t pinned_n = 0;
@@ -437,25 +437,48 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(g.tiles.ensure(n_tiles * sizeof(TileDesc)));
     TF_CUDA(g.blocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
     TF_CUDA(g.wblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
-    TF_CUDA(g.counters.ensure(nslots * 4 * sizeof(int32_t)));
+    TF_CUDA(g.xblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+    TF_CUDA(g.counters.ensure(nslots * tfb::kCounters * sizeof(int32_t)));
     TF_CUDA(g.refblk.ensure(nslots * n_tiles * sizeof(unsigned long long)));
     TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
-    TF_CUDA(cudaMemsetAsync(g.counters.p, 0, nslots * 4 * sizeof(int32_t), s));
+    TF_CUDA(cudaMemsetAsync(g.counters.p, 0, nslots * tfb::kCounters * sizeof(int32_t), s));
     TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, nslots * n_tiles * sizeof(unsigned long long), s));
     // later bands (other streams) wait on this: tile table and every slot's counters ready
     TF_CUDA(cudaEventRecord(g.ev_tables, s));
   }
-  int32_t* counters = g.counters.as<int32_t>() + 4 * bslot;
+  int32_t* counters = g.counters.as<int32_t>() + tfb::kCounters * bslot;
+  BlockDesc* xblocks = g.xblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   BlockDesc* blocks = g.blocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   BlockDesc* wblocks = g.wblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   if (want_stats) {
-    // [CTA-kernel blocks | warp-kernel blocks]
-    TF_CUDA(g.stats.ensure(2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
-    TF_CUDA(cudaMemsetAsync(g.stats.p, 0, 2 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
+    // [CTA-kernel blocks | warp-kernel blocks | EXACT (hybrid) blocks]
+    TF_CUDA(g.stats.ensure(3 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat)));
+    TF_CUDA(cudaMemsetAsync(g.stats.p, 0, 3 * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockStat), s));
   }
   const size_t frame_bytes = static_cast<size_t>(W) * H * frames;
   if (d_out != d_img && !band)
     TF_CUDA(cudaMemcpyAsync(d_out, d_img, frame_bytes, cudaMemcpyDeviceToDevice, s));
+
+  // EXACT kernel for the FAST hybrid's ill-conditioned blocks (full-spectrum CTA kernel)
+  int cfgx = -1;
+  int xsmem = 0;
+  if (!exact) {
+    cfgx = tfb::pick_config(pl.nmax, true);
+    if (cfgx >= 0) {
+      const int ntx = tfb::kCfgs[cfgx].nt, nbx = ntx * tfb::kCfgs[cfgx].bpt;
+      const tfb::SmemLayout layx(nbx, pl.wmax, p.iters, ntx / 32, nbx);
+      xsmem = layx.total;
+      if (xsmem > 227 * 1024) {
+        cfgx = -1;
+      } else if (g.occ_smem[1][cfgx] != xsmem) {
+        int occ = 0;
+        TF_CUDA(tfb::fse_prepare(cfgx, true, xsmem, &occ));
+        g.occ[1][cfgx] = occ;
+        g.occ_smem[1][cfgx] = xsmem;
+      }
+      if (cfgx >= 0 && g.occ[1][cfgx] < 1) cfgx = -1;
+    }
+  }
 
   tfb::EnumLaunch e{};
   e.known = d_known;
@@ -476,6 +499,16 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   e.warp_L = (wbpt || wide) ? span : 0;
   e.wblocks = wblocks;
   e.n_wblocks = counters + 2;
+  // FAST hybrid (TF_HYBRID = known-fraction threshold, 0 disables): blocks whose support
+  // window is almost empty of known pixels run on the EXACT kernel (config 5)
+  float hyb = 0.f;
+  if (!exact && cfgx >= 0) {
+    hyb = 0.1f;
+    if (const char* h = std::getenv("TF_HYBRID")) hyb = static_cast<float>(std::atof(h));
+  }
+  e.hyb_frac = hyb;
+  e.xblocks = xblocks;
+  e.n_xblocks = counters + 4;
   TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
 
   tfb::FseLaunch a{};
@@ -496,6 +529,18 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   a.tw = g.tw.as<double>();
   a.wmax = pl.wmax;
   a.stats = want_stats ? g.stats.as<BlockStat>() : nullptr;
+  const auto launch_x = [&](cudaStream_t st) -> int {
+    if (hyb <= 0.f) return TF_OK;
+    tfb::FseLaunch x = a;
+    x.blocks = xblocks;
+    x.n_blocks = counters + 4;
+    x.next_block = counters + 5;
+    x.stats = want_stats ? g.stats.as<BlockStat>() + 2 * static_cast<size_t>(pl.cand_blocks) : nullptr;
+    const int xg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.occ[1][cfgx],
+                                                      std::max<int64_t>(cand, 1)));
+    TF_CUDA(tfb::fse_launch(cfgx, true, x, xg, xsmem, st));
+    return TF_OK;
+  };
   int grid = g.sms * g.occ[exact][cfg];
   if (cand < grid) grid = static_cast<int>(std::max<int64_t>(1, cand));
   const int slot = static_cast<int>(g.launches % Gpu::kRing);
@@ -513,6 +558,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+    rc = launch_x(side);
+    if (rc != TF_OK) return rc;
     TF_CUDA(cudaEventRecord(g.ev_join, side));
     const int wgrid = g.sms * g.wide_occ[w64][wide];
     const size_t per = static_cast<size_t>(wgrid) * p.iters;  // log entries per band slot
@@ -546,6 +593,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     } else {
       TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
     }
+    rc = launch_x(side);
+    if (rc != TF_OK) return rc;
     TF_CUDA(cudaEventRecord(g.ev_join, side));
     tfb::FseLaunch w = a;
     w.blocks = wblocks;
@@ -567,12 +616,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
+    rc = launch_x(s);
+    if (rc != TF_OK) return rc;
   }
   if (ktime) {
     TF_CUDA(cudaStreamSynchronize(s));
-    int32_t cnt[4];
-    TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
-    std::fprintf(stderr, "[tframe] warp blocks %d, cta blocks %d\n", cnt[2], cnt[0]);
+    int32_t cnt[tfb::kCounters];
+    TF_CUDA(cudaMemcpy(cnt, counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[tframe] warp blocks %d, cta blocks %d, exact (hybrid) blocks %d\n", cnt[2],
+                 cnt[0], cnt[4]);
   }
   if (!band) {
     TF_CUDA(cudaEventRecord(g.ring1[slot], s));
@@ -585,7 +637,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     float ms = 0.f;
     TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
     res->kernel_ms = ms;
-    int32_t cnt[4];
+    int32_t cnt[tfb::kCounters];
     TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
     std::vector<unsigned long long> ref(n_tiles);
     TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, n_tiles * sizeof(unsigned long long),
@@ -593,14 +645,17 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     res->ref_blocks = 0;
     for (size_t t = 0; t < n_tiles; ++t)
       if (static_cast<int>(t % n_parts) == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
-    res->processed = cnt[0] + cnt[2];
-    std::vector<BlockStat> st(static_cast<size_t>(cnt[0] + cnt[2]));
+    res->processed = cnt[0] + cnt[2] + cnt[4];
+    std::vector<BlockStat> st(static_cast<size_t>(cnt[0] + cnt[2] + cnt[4]));
     if (cnt[0] > 0)
       TF_CUDA(cudaMemcpy(st.data(), g.stats.p, static_cast<size_t>(cnt[0]) * sizeof(BlockStat),
                          cudaMemcpyDeviceToHost));
     if (cnt[2] > 0)
       TF_CUDA(cudaMemcpy(st.data() + cnt[0], g.stats.as<BlockStat>() + pl.cand_blocks,
                          static_cast<size_t>(cnt[2]) * sizeof(BlockStat), cudaMemcpyDeviceToHost));
+    if (cnt[4] > 0)
+      TF_CUDA(cudaMemcpy(st.data() + cnt[0] + cnt[2], g.stats.as<BlockStat>() + 2 * pl.cand_blocks,
+                         static_cast<size_t>(cnt[4]) * sizeof(BlockStat), cudaMemcpyDeviceToHost));
     // algorithmic F_b = 2(4NM + 8NL) + 3N I_b + 8N (I_b + P_b) + 14 U_b T_b;
     // executed flops differ only for the FAST half-spectrum warp kernel (wkind 2), which
     // runs the row pass fully, the column pass / update / argmax on rows l <= L/2 only and
@@ -616,7 +671,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       const double f = 2.0 * (4.0 * N * b.M + 8.0 * N * b.L) + 3.0 * N * b.iters +
                        8.0 * N * (b.iters + b.pairs) + 14.0 * b.evaluated * b.touched;
       fl += f;
-      const bool warp_list = q >= static_cast<size_t>(cnt[0]);
+      const bool x_list = q >= static_cast<size_t>(cnt[0] + cnt[2]);  // EXACT (hybrid): executed == F_b
+      const bool warp_list = !x_list && q >= static_cast<size_t>(cnt[0]);
       if (pair && warp_list) {
         // pair kernel: 9 half rows x 16 columns per block, DFT as the T2 scheme
         const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
@@ -635,7 +691,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                                ? 8.0 * b.M * b.L * (b.L / 2 + 1) + 16.0 * Nh * b.M
                                : 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L;
         xfl += dft + Nh * (11.0 * b.iters + 8.0 * b.pairs) + 11.0 * b.evaluated * b.iters;
-      } else if (!warp_list && (gbpth || half)) {
+      } else if (!warp_list && !x_list && (gbpth || half)) {
         const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
         xfl += 8.0 * b.M * b.M * b.L + 16.0 * Nh * b.L + Nh * (11.0 * b.iters + 8.0 * b.pairs) +
                (gbpth ? 11.0 * b.evaluated * b.iters : 14.0 * b.evaluated * b.touched);
@@ -1058,12 +1114,14 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       float ms = 0.f;
       TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
       stats->kernel_ms = ms;
-      std::vector<int32_t> cnt(4 * static_cast<size_t>(nbands));
+      std::vector<int32_t> cnt(tfb::kCounters * static_cast<size_t>(nbands));
       TF_CUDA(cudaMemcpy(cnt.data(), g.counters.p, cnt.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
       std::vector<unsigned long long> ref(pl.tiles.size() * static_cast<size_t>(nbands));
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));
-      for (int k = 0; k < nbands; ++k) stats->blocks_processed += cnt[4 * k] + cnt[4 * k + 2];
+      for (int k = 0; k < nbands; ++k)
+        stats->blocks_processed += cnt[tfb::kCounters * k] + cnt[tfb::kCounters * k + 2] +
+                                   cnt[tfb::kCounters * k + 4];
       for (unsigned long long r : ref) stats->blocks_reference += static_cast<int64_t>(r);
     }
     return TF_OK;
@@ -1101,9 +1159,9 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       float ms = 0.f;
       TF_CUDA(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
       kms = std::max(kms, static_cast<double>(ms));
-      int32_t cnt[4];
+      int32_t cnt[tfb::kCounters];
       TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
-      stats->blocks_processed += cnt[0] + cnt[2];
+      stats->blocks_processed += cnt[0] + cnt[2] + cnt[4];
       std::vector<unsigned long long> ref(pl.tiles.size());
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));

@@ -69,7 +69,14 @@ struct EnumLaunch {
   // row band (streamed host path): only blocks whose first row, flattened over frames
   // (frame * H + halo y + block y), lies in [row0, row1) are counted and enqueued
   int64_t row0, row1;
+  // FAST hybrid: a block whose support window has a known fraction below hyb_frac goes to
+  // xblocks (run by the EXACT kernel: such windows are ill-conditioned)
+  float hyb_frac;
+  BlockDesc* xblocks;
+  int32_t* n_xblocks;
 };
+// device counters per launch slot: [n_blocks, next, n_wblocks, wnext, n_xblocks, xnext, -, -]
+constexpr int kCounters = 8;
 
 constexpr int kCY = 4;  // rows per DFT chunk
 #ifndef TF_HALF_CY
