@@ -129,6 +129,14 @@ struct Gpu {
   int wocc_smem[2][33] = {};
   bool fft_ok = false;        // c_fft32 uploaded on this device
   int pair_occ = 0, pair_smem = 0;  // FAST pair kernel (16x16 windows)
+  // CUDA graph of the device path: the second identical call (same buffers, shape, params,
+  // stream, mode and tuning environment) is captured, later identical calls replay it
+  cudaGraphExec_t gexec = nullptr;
+  std::string gkey, last_key;
+  // the same for the streamed host path (host pointers in the key; pinned buffers only)
+  cudaGraphExec_t hexec = nullptr;
+  std::string hkey, hlast;
+  cudaEvent_t ev_gstart = nullptr, ev_cout = nullptr;
   int wide_occ[3][65] = {};    // FAST wide kernel occupancy per (precision variant, window side)
   int wide_smem[3][65] = {};
   // streamed host path: copy-in / copy-out streams, a second compute stream, band events
@@ -297,7 +305,7 @@ struct Band {
 static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                       const uint8_t* d_known, int W, int H, int frames, const tf_fse_params& p,
                       int part, int n_parts, uint8_t* d_out, cudaStream_t s, bool want_stats,
-                      DevRun* res, const Band* band = nullptr) {
+                      DevRun* res, const Band* band = nullptr, bool graph = false) {
   const Band whole;
   const Band& bd = band ? *band : whole;
   const size_t bslot = static_cast<size_t>(bd.slot), nslots = static_cast<size_t>(bd.nslots);
@@ -429,8 +437,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   if (bd.first) {
     rc = upload_tables(g, p, pl.wmax, s);
     if (rc != TF_OK) return rc;
-    // table upload through pinned staging; wait for the previous upload first
-    if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
+    // table upload through pinned staging; wait for the previous upload first (a captured
+    // call was preceded by an identical call that already waited)
+    if (g.ev_tables && !graph) TF_CUDA(cudaEventSynchronize(g.ev_tables));
     rc = ensure_pinned(g, n_tiles * sizeof(TileDesc));
     if (rc != TF_OK) return rc;
     std::memcpy(g.pinned, pl.tiles.data(), n_tiles * sizeof(TileDesc));
@@ -444,7 +453,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaMemsetAsync(g.counters.p, 0, nslots * tfb::kCounters * sizeof(int32_t), s));
     TF_CUDA(cudaMemsetAsync(g.refblk.p, 0, nslots * n_tiles * sizeof(unsigned long long), s));
     // later bands (other streams) wait on this: tile table and every slot's counters ready
-    TF_CUDA(cudaEventRecord(g.ev_tables, s));
+    // (a captured call records it after the graph launch instead: an event recorded inside a
+    // capture cannot be waited on by later uncaptured calls)
+    if (!graph || band) TF_CUDA(cudaEventRecord(g.ev_tables, s));
   }
   int32_t* counters = g.counters.as<int32_t>() + tfb::kCounters * bslot;
   BlockDesc* xblocks = g.xblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
@@ -548,7 +559,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaEventCreate(&g.ring0[slot]));
     TF_CUDA(cudaEventCreate(&g.ring1[slot]));
   }
-  if (!band) {
+  if (!band && !graph) {
     TF_CUDA(cudaEventRecord(g.ev0, s));
     TF_CUDA(cudaEventRecord(g.ring0[slot], s));
   }
@@ -626,7 +637,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     std::fprintf(stderr, "[tframe] warp blocks %d, cta blocks %d, exact (hybrid) blocks %d\n", cnt[2],
                  cnt[0], cnt[4]);
   }
-  if (!band) {
+  if (!band && !graph) {
     TF_CUDA(cudaEventRecord(g.ring1[slot], s));
     TF_CUDA(cudaEventRecord(g.ev1, s));
     ++g.launches;
@@ -729,6 +740,32 @@ static int select_device(const Gpu& g) {
   return TF_OK;
 }
 
+// Any call that restages the tile table (other shapes, the host path, diffusion) invalidates
+// the device path's graph, whose memcpy node reads the pinned staging buffer.
+static int drop_graph(Gpu& g) {
+  if (g.gexec) TF_CUDA(cudaGraphExecDestroy(g.gexec));
+  g.gexec = nullptr;
+  g.gkey.clear();
+  g.last_key.clear();
+  if (g.hexec) TF_CUDA(cudaGraphExecDestroy(g.hexec));
+  g.hexec = nullptr;
+  g.hkey.clear();
+  g.hlast.clear();
+  return TF_OK;
+}
+
+// Tuning environment that changes the enqueued work (part of every graph key).
+static std::string env_key() {
+  std::string key;
+  for (const char* v : {"TF_HYBRID", "TF_WIDE_WM", "TF_NO_PAIR", "TF_NO_WIDE", "TF_NO_GEN",
+                        "TF_NO_WARP", "TF_HALF_NT", "TF_FSE_CFG", "TF_FORCE_WARP"}) {
+    const char* e = std::getenv(v);
+    key += e ? e : "-";
+    key += '|';
+  }
+  return key;
+}
+
 using clk = std::chrono::steady_clock;
 static int64_t us_since(clk::time_point a) {
   return std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - a).count();
@@ -810,6 +847,10 @@ void tf_destroy(tf_ctx* ctx) {
     cudaSetDevice(g.dev);
     if (g.stream) cudaStreamSynchronize(g.stream);
     if (g.comm && nccl().ok) nccl().CommDestroy(g.comm);
+    if (g.gexec) cudaGraphExecDestroy(g.gexec);
+    if (g.hexec) cudaGraphExecDestroy(g.hexec);
+    if (g.ev_gstart) cudaEventDestroy(g.ev_gstart);
+    if (g.ev_cout) cudaEventDestroy(g.ev_cout);
     for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
                       &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv, &g.wblocks,
                       &g.wlog_kl, &g.wlog_c, &g.qbuf})
@@ -875,6 +916,60 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
   if (rc != TF_OK) return rc;
   const int64_t plan_us = us_since(t0);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  if (!stats && !std::getenv("TF_NO_GRAPH")) {
+    // graph path: identical repeated calls (the serving / benchmark loop) replay one CUDA
+    // graph of the whole enqueue sequence, so the GPU runs it back to back without waiting
+    // for ~10 host API calls per call
+    char kb[512];
+    std::snprintf(kb, sizeof(kb), "%p %p %p %d %d %d %d %d %d %d %d %a %a %d %d %p %d|", d_img, d_known,
+                  d_out, W, H, frames, tiles, overlap, p->block, p->margin, p->iters, p->gamma, p->rho,
+                  part, n_parts, static_cast<void*>(s), ctx->mode);
+    const std::string key = std::string(kb) + env_key();
+    const bool tables_ok = g.rho_val == p->rho && g.rho_margin == p->margin && g.tw_wmax >= pl.wmax;
+    if (!(g.gexec && g.gkey == key) && g.last_key == key && tables_ok) {
+      rc = drop_graph(g);  // one graph at a time: both read the pinned tile staging
+      if (rc != TF_OK) return rc;
+      g.last_key = key;
+      cudaGraph_t graph = nullptr;
+      TF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+      rc = run_device(ctx, g, pl, d_img, d_known, W, H, frames, *p, part, n_parts, d_out, s, false,
+                      nullptr, nullptr, true);
+      const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (rc != TF_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ce != cudaSuccess) return set_error(TF_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      const cudaError_t ie = cudaGraphInstantiate(&g.gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        g.gexec = nullptr;
+        return set_error(TF_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      }
+      g.gkey = key;
+    }
+    if (g.gexec && g.gkey == key) {
+      const int slot = static_cast<int>(g.launches % Gpu::kRing);
+      if (!g.ring0[slot]) {
+        TF_CUDA(cudaEventCreate(&g.ring0[slot]));
+        TF_CUDA(cudaEventCreate(&g.ring1[slot]));
+      }
+      TF_CUDA(cudaEventRecord(g.ev0, s));
+      TF_CUDA(cudaEventRecord(g.ring0[slot], s));
+      TF_CUDA(cudaGraphLaunch(g.gexec, s));
+      TF_CUDA(cudaEventRecord(g.ev_tables, s));  // the pinned tile table is read by the graph
+      TF_CUDA(cudaEventRecord(g.ring1[slot], s));
+      TF_CUDA(cudaEventRecord(g.ev1, s));
+      ++g.launches;
+      return TF_OK;
+    }
+    rc = drop_graph(g);  // another call shape: the staged tables are about to be overwritten
+    if (rc != TF_OK) return rc;
+    g.last_key = key;
+  } else {
+    rc = drop_graph(g);
+    if (rc != TF_OK) return rc;
+  }
   DevRun dr;
   rc = run_device(ctx, g, pl, d_img, d_known, W, H, frames, *p, part, n_parts, d_out, s,
                   stats != nullptr, &dr);
@@ -906,7 +1001,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
 // of earlier ones overlap the FSE kernels; outputs are identical to the one-shot path.
 static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
                         const uint8_t* known, int W, int H, int frames, const tf_fse_params& p,
-                        uint8_t* out, int nb) {
+                        uint8_t* out, int nb, bool capture = false) {
   const auto t_start = clk::now();
   const int64_t rows = static_cast<int64_t>(frames) * H;
   const int64_t R = (rows + nb - 1) / nb;
@@ -925,8 +1020,21 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   uint8_t* di = g.img.as<uint8_t>();
   uint8_t* dk = g.known.as<uint8_t>();
   uint8_t* dout = g.out.as<uint8_t>();
-  // the previous call's copy-out must be done with g.out before it is overwritten
-  TF_CUDA(cudaStreamSynchronize(g.cout));
+  if (!g.ev_gstart) TF_CUDA(cudaEventCreateWithFlags(&g.ev_gstart, cudaEventDisableTiming));
+  if (!g.ev_cout) TF_CUDA(cudaEventCreateWithFlags(&g.ev_cout, cudaEventDisableTiming));
+  if (capture) {
+    // g.stream is capturing: fork every stream the sequence uses from it
+    TF_CUDA(cudaEventRecord(g.ev_gstart, g.stream));
+    TF_CUDA(cudaStreamWaitEvent(g.cin, g.ev_gstart, 0));
+    TF_CUDA(cudaStreamWaitEvent(g.cout, g.ev_gstart, 0));
+    for (int k = 0; k < nb; ++k) {
+      TF_CUDA(cudaStreamWaitEvent(g.bs[k], g.ev_gstart, 0));
+      TF_CUDA(cudaStreamWaitEvent(g.bside[k], g.ev_gstart, 0));
+    }
+  } else {
+    // the previous call's copy-out must be done with g.out before it is overwritten
+    TF_CUDA(cudaStreamSynchronize(g.cout));
+  }
   // copy-in in finer chunks than the compute bands: a band waits only for the chunk that
   // holds the last row its windows reach
   // holds the last row its windows reach.  Chunks are enqueued just ahead of the first band
@@ -971,9 +1079,9 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     int rc = copy_in_upto(need);
     if (rc != TF_OK) return rc;
     TF_CUDA(cudaStreamWaitEvent(cs, g.ev_in[need], 0));
-    if (k == 0) TF_CUDA(cudaEventRecord(g.ev0, cs));
+    if (k == 0 && !capture) TF_CUDA(cudaEventRecord(g.ev0, cs));
     if (k > 0) TF_CUDA(cudaStreamWaitEvent(cs, g.ev_tables, 0));  // tile table + counters
-    rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b);
+    rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b, capture);
     if (rc != TF_OK) return rc;
     TF_CUDA(cudaEventRecord(g.ev_done[k], cs));
   }
@@ -990,8 +1098,13 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     TF_CUDA(cudaMemcpyAsync(out + off, dout + off, n, cudaMemcpyDeviceToHost, g.cout));
   }
   for (int k = 0; k < nb; ++k) TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_done[k], 0));
-  TF_CUDA(cudaEventRecord(g.ev1, g.stream));
   g.last_slots = nb;
+  if (capture) {  // join the copy-out (and through the band events every stream) back
+    TF_CUDA(cudaEventRecord(g.ev_cout, g.cout));
+    TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_cout, 0));
+    return TF_OK;
+  }
+  TF_CUDA(cudaEventRecord(g.ev1, g.stream));
   const auto t_enq = clk::now();
   TF_CUDA(cudaStreamSynchronize(g.cout));
   TF_CUDA(cudaStreamSynchronize(g.stream));
@@ -1077,6 +1190,13 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
   if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
   int rc = check_params(p);
   if (rc != TF_OK) return rc;
+  for (Gpu& gd : ctx->gpus) {  // this restages the tile table: the device path's graph is stale
+    TF_CUDA(cudaSetDevice(gd.dev));
+    if (gd.gexec) TF_CUDA(cudaGraphExecDestroy(gd.gexec));
+    gd.gexec = nullptr;
+    gd.gkey.clear();
+    gd.last_key.clear();
+  }
   const auto t0 = clk::now();
   Plan pl;
   rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
@@ -1103,7 +1223,59 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     rc = select_device(g);
     if (rc != TF_OK) return rc;
     const auto t_d = clk::now();
-    rc = run_streamed(ctx, g, pl, img, known, W, H, frames, *p, out, nbands);
+    // graph path (as the device path): the second identical call with pinned host buffers
+    // is captured, later identical calls replay it with one launch
+    const auto pinned = [](const void* q) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return at.type == cudaMemoryTypeHost;
+    };
+    std::string key;
+    if (!std::getenv("TF_NO_GRAPH") && pinned(img) && pinned(known) && pinned(out)) {
+      char kb[512];
+      std::snprintf(kb, sizeof(kb), "%p %p %p %d %d %d %d %d %d %d %d %a %a %d %d|",
+                    static_cast<const void*>(img), static_cast<const void*>(known),
+                    static_cast<void*>(out), W, H, frames, tiles, overlap, p->block, p->margin,
+                    p->iters, p->gamma, p->rho, ctx->mode, nbands);
+      key = std::string(kb) + env_key();
+    }
+    const bool tables_ok = g.rho_val == p->rho && g.rho_margin == p->margin && g.tw_wmax >= pl.wmax;
+    if (!key.empty() && !(g.hexec && g.hkey == key) && g.hlast == key && tables_ok) {
+      rc = drop_graph(g);
+      if (rc != TF_OK) return rc;
+      TF_CUDA(cudaStreamSynchronize(g.cout));  // previous call's copy-out (outside the capture)
+      cudaGraph_t graph = nullptr;
+      TF_CUDA(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeRelaxed));
+      rc = run_streamed(ctx, g, pl, img, known, W, H, frames, *p, out, nbands, true);
+      const cudaError_t ce = cudaStreamEndCapture(g.stream, &graph);
+      if (rc != TF_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ce != cudaSuccess) return set_error(TF_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      const cudaError_t ie = cudaGraphInstantiate(&g.hexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        g.hexec = nullptr;
+        return set_error(TF_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      }
+      g.hkey = key;
+    }
+    if (!key.empty() && g.hexec && g.hkey == key) {
+      TF_CUDA(cudaEventRecord(g.ev0, g.stream));
+      TF_CUDA(cudaGraphLaunch(g.hexec, g.stream));
+      TF_CUDA(cudaEventRecord(g.ev_tables, g.stream));  // host-waitable again after the capture
+      TF_CUDA(cudaEventRecord(g.ev1, g.stream));
+      TF_CUDA(cudaStreamSynchronize(g.stream));
+    } else {
+      rc = drop_graph(g);
+      if (rc != TF_OK) return rc;
+      g.hlast = key;
+      rc = run_streamed(ctx, g, pl, img, known, W, H, frames, *p, out, nbands);
+    }
     if (rc != TF_OK) return rc;
     if (stats) {
       *stats = tf_run_stats{};
@@ -1125,6 +1297,11 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       for (unsigned long long r : ref) stats->blocks_reference += static_cast<int64_t>(r);
     }
     return TF_OK;
+  }
+  for (Gpu& gd : ctx->gpus) {  // the one-shot path restages the tables: no graph stays valid
+    TF_CUDA(cudaSetDevice(gd.dev));
+    rc = drop_graph(gd);
+    if (rc != TF_OK) return rc;
   }
   // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
   std::vector<DevRun> dr(static_cast<size_t>(n));
@@ -1242,6 +1419,11 @@ int tf_tiled_diffusion(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
   if (!img || !known || !out) return set_error(TF_EINVAL, "null buffer");
   int rc = check_diffusion(iters);
   if (rc != TF_OK) return rc;
+  for (Gpu& gd : ctx->gpus) {  // these restage the tile table: the device path's graph is stale
+    TF_CUDA(cudaSetDevice(gd.dev));
+    rc = drop_graph(gd);
+    if (rc != TF_OK) return rc;
+  }
   const auto t0 = clk::now();
   Plan pl;
   rc = make_plan(W, H, frames, tiles, overlap, 1, 0, pl);  // block grid unused

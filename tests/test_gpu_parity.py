@@ -325,3 +325,71 @@ def test_fast_hybrid_routes_ill_conditioned_blocks(ctx, fctx, monkeypatch):
     w0 = (np.abs(ex.astype(int) - fa0.astype(int))[unk] <= 1).mean()
     w1 = (np.abs(ex.astype(int) - fa1.astype(int))[unk] <= 1).mean()
     assert w1 >= FAST_WITHIN1 > w0, (w0, w1)
+
+
+def test_device_path_graph_replay_tracks_inputs_and_shapes(fctx):
+    """Repeated identical device-path calls are captured once and replayed as a CUDA graph:
+    new contents of the same buffers must be picked up, and a call of another shape (or the
+    host path) in between must not leave a stale graph behind."""
+    import torch
+    wl = CONFIGS[2]
+    W, H = 480, 270
+    frames = [T.synth_frame(2, f, W, H) for f in range(4)]
+    d_img = torch.empty(H * W, dtype=torch.uint8, device="cuda")
+    d_kn = torch.empty_like(d_img)
+    d_out = torch.empty_like(d_img)
+    s = torch.cuda.Stream()
+
+    def dev_call(img, kn, tiles=wl.tiles):
+        d_img.copy_(torch.from_numpy(img.reshape(-1)))
+        d_kn.copy_(torch.from_numpy(kn.reshape(-1)))
+        torch.cuda.synchronize()
+        fctx.tiled_device(d_img.data_ptr(), d_kn.data_ptr(), d_out.data_ptr(), W, H, 1, tiles, wl.overlap,
+                          wl.params, stream=s.cuda_stream)
+        s.synchronize()
+        return d_out.cpu().numpy().reshape(H, W)
+
+    for rep in range(3):
+        for img, kn in frames:  # repeated identical calls on new data (graph replays)
+            want, _ = fctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+            for _ in range(3):
+                got = dev_call(img, kn)
+                assert np.array_equal(got, want)
+        img, kn = frames[0]
+        want3, _ = fctx.tiled(img, kn, 3, wl.overlap, wl.params)
+        assert np.array_equal(dev_call(img, kn, tiles=3), want3)  # another shape in between
+
+
+def test_host_path_graph_replay_tracks_inputs(fctx, ctx):
+    """Repeated identical host-buffer calls (pinned buffers) are captured once and replayed:
+    the replays must read the current contents of the same host buffers, and calls of other
+    shapes / the device path in between must not leave a stale graph."""
+    import torch
+    wl = CONFIGS[2]
+    W, H = 960, 540
+    frames = [T.synth_frame(2, f, W, H) for f in range(3)]
+    h_img = torch.empty(H * W, dtype=torch.uint8).pin_memory()
+    h_kn = torch.empty_like(h_img).pin_memory()
+    h_out = torch.empty_like(h_img).pin_memory()
+    import ctypes as C
+    from paper_2207_00238_b200 import _native as N
+    p = wl.params._c()
+
+    def host_call(c, img, kn, tiles=wl.tiles):
+        h_img.numpy()[:] = img.reshape(-1)
+        h_kn.numpy()[:] = kn.reshape(-1)
+        N.check(N.lib().tf_tiled_extrapolate(c.handle, h_img.data_ptr(), h_kn.data_ptr(), W, H, 1, tiles,
+                                             wl.overlap, C.byref(p), h_out.data_ptr(), None))
+        return h_out.numpy().reshape(H, W).copy()
+
+    for rep in range(2):
+        for img, kn in frames:
+            want = O.tiled(img, kn, wl.tiles, wl.overlap, p.block, p.margin, p.iters, p.gamma, p.rho)[0]
+            got = [host_call(ctx, img, kn) for _ in range(3)]  # EXACT: byte-identical every replay
+            for g in got:
+                assert np.array_equal(g, want)
+            fa = [host_call(fctx, img, kn) for _ in range(3)]
+            assert all(np.array_equal(f, fa[0]) for f in fa)
+        img, kn = frames[0]
+        want3 = O.tiled(img, kn, 3, wl.overlap, p.block, p.margin, p.iters, p.gamma, p.rho)[0]
+        assert np.array_equal(host_call(ctx, img, kn, tiles=3), want3)
