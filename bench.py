@@ -365,7 +365,9 @@ def main():
         "e2e": {"value": round(e2e, 3), "unit": "Mpixel/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb,
                 "path": "tf_tiled_extrapolate (host buffers, streamed row bands), per rank"},
-        "gpu_launches": args.steps * 3,  # enumerate + warp-per-block FSE + border-window FSE per step
+        # per step, FAST: enumerate + half-spectrum FSE + border-window (GEN) FSE + the hybrid's
+        # EXACT kernel (empty list on c2); EXACT: enumerate + CTA FSE
+        "gpu_launches": args.steps * (4 if args.mode == "fast" else 2),
         "roofline": roof,
         "clocks": res["clocks"],
         other + "_mode": {"value": round(world * fb / (res_other["ms_step"] * 1e-3) / 1e6, 3),
