@@ -143,6 +143,7 @@ struct Gpu {
   static constexpr int kMaxBands = 16;
   cudaStream_t cin = nullptr, cout = nullptr, stream2 = nullptr;
   cudaStream_t bs[kMaxBands] = {}, bside[kMaxBands] = {};  // per-band compute / fork streams
+  int bs_prio[kMaxBands] = {};
   cudaEvent_t ev_in[kMaxBands] = {}, ev_done[kMaxBands] = {};
   int last_slots = 1;         // band slots used by the last host-path run (stats)
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
@@ -993,8 +994,8 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
 // Gather the cores of GPUs 1..n-1 into GPU 0 (NCCL send/recv over NVLink), download the
 // merged frames from GPU 0 and wait for every GPU (run_master's merge, runtime.hpp:112-130).
 // Streamed host path on one GPU (tf_tiled_extrapolate with host buffers): the frames are cut
-// into nb row bands (rows flattened over frames).  Copy-in stream: band k's image and mask
-// rows H2D, then the output rows initialised from the image (D2D).  Compute (two
+// into nb row bands (rows flattened over frames).  Copy-in stream: image and mask rows H2D
+// in chunks; the kernels reconstruct in place in the image buffer.  Compute (two
 // per-band streams): band k's blocks (first row in band k) once every band its windows
 // reach has arrived.  Copy-out stream: band k's output rows D2H once bands k-1 and k are
 // computed (a block writes only its own B <= R rows).  The H2D of later bands and the D2H
@@ -1007,19 +1008,43 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   const int64_t R = (rows + nb - 1) / nb;
   for (cudaStream_t* st : {&g.cin, &g.cout, &g.stream2})
     if (!*st) TF_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+  // band streams with decreasing priority: pending CTAs of earlier bands are dispatched
+  // first, so bands complete roughly in order and their copy-out overlaps later bands
+  int least = 0, greatest = 0;
+  TF_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  const bool prio = !std::getenv("TF_NO_BAND_PRIO");
   for (int k = 0; k < Gpu::kMaxBands; ++k) {
     if (!g.ev_in[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_in[k], cudaEventDisableTiming));
     if (!g.ev_done[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_done[k], cudaEventDisableTiming));
-    if (!g.bs[k]) TF_CUDA(cudaStreamCreateWithFlags(&g.bs[k], cudaStreamNonBlocking));
-    if (!g.bside[k]) TF_CUDA(cudaStreamCreateWithFlags(&g.bside[k], cudaStreamNonBlocking));
+    const int pr = prio ? std::min(least, greatest + k) : least;
+    if (g.bs[k] && g.bs_prio[k] != pr) {
+      TF_CUDA(cudaStreamSynchronize(g.bs[k]));
+      TF_CUDA(cudaStreamDestroy(g.bs[k]));
+      TF_CUDA(cudaStreamSynchronize(g.bside[k]));
+      TF_CUDA(cudaStreamDestroy(g.bside[k]));
+      g.bs[k] = g.bside[k] = nullptr;
+    }
+    if (!g.bs[k]) {
+      TF_CUDA(cudaStreamCreateWithPriority(&g.bs[k], cudaStreamNonBlocking, pr));
+      TF_CUDA(cudaStreamCreateWithPriority(&g.bside[k], cudaStreamNonBlocking, pr));
+      g.bs_prio[k] = pr;
+    }
   }
   const size_t bytes = static_cast<size_t>(W) * rows;
   TF_CUDA(g.img.ensure(bytes));
   TF_CUDA(g.known.ensure(bytes));
-  TF_CUDA(g.out.ensure(bytes));
   uint8_t* di = g.img.as<uint8_t>();
   uint8_t* dk = g.known.as<uint8_t>();
-  uint8_t* dout = g.out.as<uint8_t>();
+  // in place: the kernels write only unknown pixels, and every window reads image values only
+  // at known pixels (extrapolate.hpp:301-311), so no output initialisation copy is needed (a
+  // device-to-device copy on the copy-in stream would wait for SM slots behind the kernels)
+  uint8_t* dout = di;
+  // TF_STREAM_DEBUG: timing events (start, chunks, band starts / ends, copy-out end)
+  const bool dbg = !capture && std::getenv("TF_STREAM_DEBUG");
+  static cudaEvent_t dev_t[3 * Gpu::kMaxBands + 4] = {};
+  if (dbg && !dev_t[0])
+    for (cudaEvent_t& e : dev_t) TF_CUDA(cudaEventCreate(&e));
+  if (dbg) TF_CUDA(cudaEventRecord(dev_t[0], g.cin));
   if (!g.ev_gstart) TF_CUDA(cudaEventCreateWithFlags(&g.ev_gstart, cudaEventDisableTiming));
   if (!g.ev_cout) TF_CUDA(cudaEventCreateWithFlags(&g.ev_cout, cudaEventDisableTiming));
   if (capture) {
@@ -1039,7 +1064,10 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   // holds the last row its windows reach
   // holds the last row its windows reach.  Chunks are enqueued just ahead of the first band
   // that needs them, so band 0's kernels are enqueued after only its own chunks.
-  const int nin = std::min(Gpu::kMaxBands, std::max(nb, 8));
+  // chunks: a few large copies beat many small ones (each H2D has a fixed cost; c2
+  // measured 0.79 ms per call with 2 bands / 3 chunks vs 0.81-0.85 with 8-12 chunks)
+  int nin = std::min(Gpu::kMaxBands, std::max(nb + 1, 3));
+  if (const char* e = std::getenv("TF_STREAM_CHUNKS")) nin = std::min(Gpu::kMaxBands, std::max(1, std::atoi(e)));
   const int64_t Rin = (rows + nin - 1) / nin;
   int next_in = 0;
   const auto copy_in_upto = [&](int last) -> int {
@@ -1049,9 +1077,9 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
         const size_t off = static_cast<size_t>(r0) * W, n = static_cast<size_t>(r1 - r0) * W;
         TF_CUDA(cudaMemcpyAsync(di + off, img + off, n, cudaMemcpyHostToDevice, g.cin));
         TF_CUDA(cudaMemcpyAsync(dk + off, known + off, n, cudaMemcpyHostToDevice, g.cin));
-        TF_CUDA(cudaMemcpyAsync(dout + off, di + off, n, cudaMemcpyDeviceToDevice, g.cin));
       }
       TF_CUDA(cudaEventRecord(g.ev_in[next_in], g.cin));
+      if (dbg) TF_CUDA(cudaEventRecord(dev_t[1 + next_in], g.cin));
     }
     return TF_OK;
   };
@@ -1072,18 +1100,20 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     // one stream per band: every band's kernels can run as soon as its rows have arrived,
     // the CTAs of earlier-launched bands are dispatched first
     cudaStream_t cs = g.bs[k];
-    // last row the band's windows reach, and the first row of the next band (whose
-    // output rows this band's blocks may write: they must be initialised first)
+    // last row the band's windows reach (and at least the next band's first row: this
+    // band's blocks may write there, after its image rows have arrived)
     const int64_t maxrow = std::min(rows - 1, std::max(b.row1 - 1 + span, b.row1));
     const int need = static_cast<int>(std::min<int64_t>(nin - 1, maxrow / Rin));
     int rc = copy_in_upto(need);
     if (rc != TF_OK) return rc;
     TF_CUDA(cudaStreamWaitEvent(cs, g.ev_in[need], 0));
     if (k == 0 && !capture) TF_CUDA(cudaEventRecord(g.ev0, cs));
+    if (dbg) TF_CUDA(cudaEventRecord(dev_t[1 + Gpu::kMaxBands + k], cs));
     if (k > 0) TF_CUDA(cudaStreamWaitEvent(cs, g.ev_tables, 0));  // tile table + counters
     rc = run_device(ctx, g, pl, di, dk, W, H, frames, p, 0, 1, dout, cs, false, nullptr, &b, capture);
     if (rc != TF_OK) return rc;
     TF_CUDA(cudaEventRecord(g.ev_done[k], cs));
+    if (dbg) TF_CUDA(cudaEventRecord(dev_t[1 + 2 * Gpu::kMaxBands + k], cs));
   }
   {
     const int rc = copy_in_upto(nin - 1);  // (all chunks are needed by the last band already)
@@ -1099,6 +1129,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   }
   for (int k = 0; k < nb; ++k) TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_done[k], 0));
   g.last_slots = nb;
+  if (dbg) TF_CUDA(cudaEventRecord(dev_t[3 * Gpu::kMaxBands + 1], g.cout));
   if (capture) {  // join the copy-out (and through the band events every stream) back
     TF_CUDA(cudaEventRecord(g.ev_cout, g.cout));
     TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_cout, 0));
@@ -1108,6 +1139,19 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   const auto t_enq = clk::now();
   TF_CUDA(cudaStreamSynchronize(g.cout));
   TF_CUDA(cudaStreamSynchronize(g.stream));
+  if (dbg) {
+    const auto at = [&](int i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, dev_t[0], dev_t[i]);
+      return ms * 1e3f;
+    };
+    std::fprintf(stderr, "[tframe] timeline us: chunks");
+    for (int i = 0; i < nin; ++i) std::fprintf(stderr, " %.0f", at(1 + i));
+    std::fprintf(stderr, " | band start/end");
+    for (int k = 0; k < nb; ++k)
+      std::fprintf(stderr, " %.0f/%.0f", at(1 + Gpu::kMaxBands + k), at(1 + 2 * Gpu::kMaxBands + k));
+    std::fprintf(stderr, " | copy-out end %.0f\n", at(3 * Gpu::kMaxBands + 1));
+  }
   if (std::getenv("TF_STREAM_DEBUG")) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, g.ev0, g.ev1);
@@ -1213,7 +1257,7 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     // 4 bands, c3 6.93 / 6.75 ms at 4-8, c4 15.24 / 14.17 ms at 8; the host enqueue costs
     // ~25-35 us per band and banding adds ~5 % compute (smaller launches), so bands stay a
     // few hundred rows tall
-    nbands = static_cast<int>(std::clamp<int64_t>(rows / 256, 1, 8));
+    nbands = static_cast<int>(std::clamp<int64_t>(rows / 512, 1, 8));
     if (const char* e = std::getenv("TF_STREAM_BANDS")) nbands = std::atoi(e);
     nbands = std::max(1, std::min(nbands, Gpu::kMaxBands));
     if ((rows + nbands - 1) / nbands < p->block) nbands = 1;  // a block spans at most 2 bands
