@@ -393,3 +393,28 @@ def test_host_path_graph_replay_tracks_inputs(fctx, ctx):
         img, kn = frames[0]
         want3 = O.tiled(img, kn, 3, wl.overlap, p.block, p.margin, p.iters, p.gamma, p.rho)[0]
         assert np.array_equal(host_call(ctx, img, kn, tiles=3), want3)
+
+
+GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+GOLD_FSE = sorted(p.name for p in GOLD.glob("*.npz") if p.name != "tiling.npz")
+
+
+@pytest.mark.parametrize("name", GOLD_FSE)
+def test_gpu_reproduces_reference_golden_fixtures(ctx, fctx, name):
+    """The committed fixtures the reference itself produced (tests/golden/make_golden.py):
+    EXACT byte-identical, FAST within the north-star tolerance, block counts equal."""
+    d = np.load(GOLD / name)
+    b, m, i = (int(v) for v in d["params"])
+    g, r = (float(v) for v in d["fparams"])
+    p = T.FseLiteParams(b, m, i, g, r)
+    tiles, overlap = int(d["tiles"]), int(d["overlap"])
+    got, st = ctx.tiled(d["img"], d["known"], tiles, overlap, p)
+    assert np.array_equal(got, d["out"]), f"{name}: {(got != d['out']).sum()} px differ"
+    if tiles == 1 and overlap == 0:
+        assert st.blocks_reference == int(d["nblocks"])  # FseLiteTrace block count
+    fa, _ = fctx.tiled(d["img"], d["known"], tiles, overlap, p)
+    unk = d["known"] == 0
+    if unk.any():
+        dd = np.abs(fa.astype(int) - d["out"].astype(int))[unk]
+        assert (dd <= 1).mean() >= FAST_WITHIN1 or dd.size < 1000 and (dd <= 1).mean() >= 0.99, name
+    assert np.array_equal(fa[~unk], d["img"][~unk])
