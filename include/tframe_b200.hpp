@@ -194,4 +194,31 @@ inline tf_rect expand(const tf_rect& core, int d, int W, int H) {
   return h;
 }
 
+// metrics.hpp:12-90 on the GPU (tf_quality*): same names and errors as the reference
+inline double mse(Context& ctx, const std::vector<uint8_t>& a, const std::vector<uint8_t>& b, int w,
+                  int h) {
+  double v = 0.0;
+  check(tf_mse(ctx.get(), a.data(), b.data(), w, h, &v));
+  return v;
+}
+inline double mse_missing(Context& ctx, const std::vector<uint8_t>& a, const std::vector<uint8_t>& b,
+                          const std::vector<uint8_t>& known, int w, int h) {
+  double v = 0.0;
+  check(tf_mse_missing(ctx.get(), a.data(), b.data(), known.data(), w, h, &v));
+  return v;
+}
+inline double psnr_from_mse(double m) { return tf_psnr_from_mse(m); }
+inline double psnr(Context& ctx, const std::vector<uint8_t>& a, const std::vector<uint8_t>& b, int w,
+                   int h) {
+  double v = 0.0;
+  check(tf_psnr(ctx.get(), a.data(), b.data(), w, h, &v));
+  return v;
+}
+inline double ssim(Context& ctx, const std::vector<uint8_t>& a, const std::vector<uint8_t>& b, int w,
+                   int h) {
+  double v = 0.0;
+  check(tf_ssim(ctx.get(), a.data(), b.data(), w, h, &v));
+  return v;
+}
+
 }  // namespace tfb200

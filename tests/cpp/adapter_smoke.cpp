@@ -34,6 +34,16 @@ int main() {
     kn[500] = 0;
     const auto out = ex.extrapolate(img, kn, 32, 32);
     if (out[500] != 100) return 6;
+    tfb200::Context ctx;
+    std::vector<uint8_t> b = img;
+    b[3] = 110;
+    if (tfb200::mse(ctx, img, b, 32, 32) != 100.0 / 1024.0) return 7;
+    if (!(tfb200::ssim(ctx, img, img, 32, 32) == 1.0)) return 8;
+    try {
+      tfb200::mse_missing(ctx, img, b, std::vector<uint8_t>(32 * 32, 1), 32, 32);
+      return 9;
+    } catch (const std::invalid_argument&) {
+    }
   }
   std::printf("adapter ok (%d GPUs)\n", n);
   return 0;
