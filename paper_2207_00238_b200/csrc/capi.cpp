@@ -141,7 +141,8 @@ struct Gpu {
   int wide_smem[3][65] = {};
   // streamed host path: copy-in / copy-out streams, a second compute stream, band events
   static constexpr int kMaxBands = 16;
-  cudaStream_t cin = nullptr, cout = nullptr, stream2 = nullptr;
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t dbg_ev[3 * kMaxBands + 4] = {};  // TF_STREAM_DEBUG timeline events
   cudaStream_t bs[kMaxBands] = {}, bside[kMaxBands] = {};  // per-band compute / fork streams
   int bs_prio[kMaxBands] = {};
   cudaEvent_t ev_in[kMaxBands] = {}, ev_done[kMaxBands] = {};
@@ -868,7 +869,9 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.ev_fork) cudaEventDestroy(g.ev_fork);
     if (g.ev_join) cudaEventDestroy(g.ev_join);
     if (g.side) cudaStreamDestroy(g.side);
-    for (cudaStream_t* st : {&g.cin, &g.cout, &g.stream2})
+    for (cudaEvent_t e : g.dbg_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t* st : {&g.cin, &g.cout})
       if (*st) {
         cudaStreamSynchronize(*st);
         cudaStreamDestroy(*st);
@@ -1006,7 +1009,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   const auto t_start = clk::now();
   const int64_t rows = static_cast<int64_t>(frames) * H;
   const int64_t R = (rows + nb - 1) / nb;
-  for (cudaStream_t* st : {&g.cin, &g.cout, &g.stream2})
+  for (cudaStream_t* st : {&g.cin, &g.cout})
     if (!*st) TF_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
   // band streams with decreasing priority: pending CTAs of earlier bands are dispatched
   // first, so bands complete roughly in order and their copy-out overlaps later bands
@@ -1041,9 +1044,9 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   uint8_t* dout = di;
   // TF_STREAM_DEBUG: timing events (start, chunks, band starts / ends, copy-out end)
   const bool dbg = !capture && std::getenv("TF_STREAM_DEBUG");
-  static cudaEvent_t dev_t[3 * Gpu::kMaxBands + 4] = {};
+  cudaEvent_t* dev_t = g.dbg_ev;
   if (dbg && !dev_t[0])
-    for (cudaEvent_t& e : dev_t) TF_CUDA(cudaEventCreate(&e));
+    for (cudaEvent_t& e : g.dbg_ev) TF_CUDA(cudaEventCreate(&e));
   if (dbg) TF_CUDA(cudaEventRecord(dev_t[0], g.cin));
   if (!g.ev_gstart) TF_CUDA(cudaEventCreateWithFlags(&g.ev_gstart, cudaEventDisableTiming));
   if (!g.ev_cout) TF_CUDA(cudaEventCreateWithFlags(&g.ev_cout, cudaEventDisableTiming));
