@@ -5,6 +5,7 @@ import sys
 
 sys.path.insert(0, '.')
 os.environ.setdefault('TF_STREAM_BANDS', '1')
+os.environ.setdefault('TF_HYBRID', '0')  # raw FAST: what the hybrid would have to fix
 import numpy as np
 
 from paper_2207_00238_b200 import tframe as T
