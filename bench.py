@@ -161,7 +161,7 @@ def ncu_profile(mode):
     if not files:
         return {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    traffic, smem, found = 0.0, [], False
+    traffic, smem, found, fp64, pipe = 0.0, [], False, None, []
     with open(files[-1]) as f:
         rows = list(csv.DictReader(f))
     for r in rows:
@@ -172,9 +172,14 @@ def ncu_profile(mode):
             found = True
         if r["metric"] == "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed":
             smem.append(round(float(r["value"]), 1))
+        if r["metric"] == "derived_fp64_flops":
+            fp64 = (fp64 or 0.0) + float(r["value"])
+        if r["metric"] == "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active":
+            pipe.append(round(float(r["value"]), 1))
     if not found:
         return {}
-    return {"traffic": int(traffic), "smem_pct": smem, "source": Path(files[-1]).name}
+    return {"traffic": int(traffic), "smem_pct": smem, "source": Path(files[-1]).name,
+            "fp64_flops": fp64, "fp64_pipe_pct": pipe}
 
 
 def main():
@@ -326,6 +331,13 @@ def main():
             "traffic": prof.get("traffic"),
             "traffic_source": prof.get("source"),
             "smem_wavefront_pct_of_peak_ncu": prof.get("smem_pct"),
+            # FP64-only view from the committed ncu capture: FP64 flops the FSE kernels
+            # executed (packed FP32 excluded) over this run's FSE time, and the FP64 pipe's
+            # utilisation per kernel — the kernels are latency/issue-bound, not FP64-pipe-bound
+            "ncu_fp64_flops_per_launch": prof.get("fp64_flops"),
+            "ncu_fp64_tflops": (round(prof["fp64_flops"] / (mean_k * 1e-3) / 1e12, 3)
+                                if prof.get("fp64_flops") else None),
+            "fp64_pipe_pct_of_peak_ncu": prof.get("fp64_pipe_pct"),
             "peak_source": "FP64 DFMA rate measured live by tf_calibrate (MEASURED_PEAKS.json has no FP64 figure)",
             "fse_kernel_ms": round(mean_k, 4), "flops_executed_per_launch": st.flops_executed,
             "flops_algorithmic_per_launch": st.flops,

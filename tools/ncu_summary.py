@@ -43,6 +43,18 @@ def full(rep, out):
             for k in KEYS:
                 if k in d:
                     w.writerow([d["Kernel Name"], k, d[k], u.get(k, "")])
+            # FP64 flops the launch executed: (2 DFMA + DADD + DMUL) thread instructions, from
+            # their per-elapsed-cycle rates x elapsed cycles (packed FP32 FFMA2/FADD2/FMUL2
+            # have no thread-instruction counter here and are not included)
+            try:
+                rate = sum(m * float(d[f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"])
+                           for op, m in (("dfma", 2), ("dadd", 1), ("dmul", 1)))
+                dur = float(d["gpu__time_duration.sum"]) * {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(
+                    u.get("gpu__time_duration.sum", "usecond"), 1e-6)
+                hz = float(d["sm__cycles_elapsed.avg.per_second"]) * 1e9  # GHz
+                w.writerow([d["Kernel Name"], "derived_fp64_flops", f"{rate * dur * hz:.6g}", "flop"])
+            except (KeyError, ValueError):
+                pass
 
 
 def launches(src, out):
