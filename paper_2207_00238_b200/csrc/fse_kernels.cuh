@@ -72,6 +72,7 @@ struct EnumLaunch {
   // FAST hybrid: a block whose support window has a known fraction below hyb_frac goes to
   // xblocks (run by the EXACT kernel: such windows are ill-conditioned)
   float hyb_frac;
+  float hyb_ratio;            // ... or fewer known window pixels than hyb_ratio x the block's unknown ones
   BlockDesc* xblocks;
   int32_t* n_xblocks;
 };
