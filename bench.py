@@ -144,20 +144,20 @@ def run_reference(args, wl, rank, world):
         "config": {"workload": wl.describe(), "frames_per_step": 1},
         "cpu_baseline": {"value": round(v, 3), "unit": "Mpixel/s", "cores": info["threads"],
                          "kind": "reference",
-                         "sample": f"full c2 frame per step ({wl.W}x{wl.H}, {wl.tiles} tiles, d={wl.overlap}), "
+                         "sample": f"full c{wl.config} frame per step ({wl.W}x{wl.H}, {wl.tiles} tiles, d={wl.overlap}), "
                                    "bit-exact B-aligned band split over all host threads"},
         "e2e": {"value": round(v, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def ncu_profile(mode):
+def ncu_profile(mode, config=CONFIG):
     """DRAM bytes (read + write) per launch of the FSE kernels and their shared-memory
     wavefront utilisation, from the committed `ncu --set full` summary of this workload
     (profiles/rNN_ncu_fse_c2_<mode>_summary.csv, written by tools/ncu_summary.py)."""
     import csv
     import glob
-    files = sorted(glob.glob(str(ROOT / "profiles" / f"r*_ncu_fse_c2_{mode}_summary.csv")))
+    files = sorted(glob.glob(str(ROOT / "profiles" / f"r*_ncu_*_c{config}_{mode}_summary.csv")))
     if not files:
         return {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -191,6 +191,9 @@ def main():
     ap.add_argument("--mode", default=os.environ.get("TF_BENCH_MODE", "fast"), choices=["exact", "fast"],
                     help="headline arithmetic mode; the other mode is timed and reported too")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=CONFIG, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config (default 2, the one the metric is quoted on; the others "
+                         "for the per-config evidence in profiles/)")
     args = ap.parse_args()
 
     rank = _env_int("RANK", 0)
@@ -198,7 +201,7 @@ def main():
     local = _env_int("LOCAL_RANK", 0)
 
     from paper_2207_00238_b200.configs import workload
-    wl = workload(CONFIG)
+    wl = workload(args.config)
 
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
@@ -325,7 +328,7 @@ def main():
     st = res["stats"]
     mean_k = res["fse_ms"]
     achieved = st.flops_executed / (mean_k * 1e-3) / 1e12
-    prof = ncu_profile(args.mode)
+    prof = ncu_profile(args.mode, args.config)
     roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64.value, 3),
             "unit": "TFLOP/s", "frac": round(achieved / fp64.value, 4),
             "traffic": prof.get("traffic"),
@@ -369,7 +372,7 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (versioned generator v1, per-rank seed 1000*2+rank)",
+        "data": f"synthetic (versioned generator v1, per-rank seed 1000*{wl.config}+rank)",
         "config": {"workload": wl.describe(), "frames_per_gpu_per_step": 1, "mode": args.mode,
                    "l2": "flushed between steps (256 MiB write outside the timed events)",
                    "parallelism": f"dp{world} frames, NCCL gather to rank 0" if world > 1 else "single GPU",
@@ -397,7 +400,7 @@ def main():
                 line["cpu_baseline"] = {
                     "value": round(v, 3), "unit": "Mpixel/s", "cores": info["threads"],
                     "kind": "reference",
-                    "sample": f"one full c2 frame ({W}x{H}), reference FSE-lite via bit-exact band split",
+                    "sample": f"one full c{wl.config} frame ({W}x{H}), reference FSE-lite via bit-exact band split",
                 }
                 line["parity"]["exact_bytes_equal_reference"] = bool(np.array_equal(ref_out, ex_out))
                 dr = np.abs(ref_out.astype(int) - fa_out.astype(int))[unk]
