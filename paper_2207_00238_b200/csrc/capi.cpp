@@ -570,13 +570,22 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaEventRecord(g.ev0, s));
     TF_CUDA(cudaEventRecord(g.ring0[slot], s));
   }
+  // the hybrid's EXACT kernel first, on the launch stream, before the FSE kernels: an empty
+  // list then costs a launch; launched concurrently on a fork (before or after them) even an
+  // empty list cost c2 5-11 % (its CTAs competed for SM slots with the persistent FSE
+  // kernels), and after them on the stream 5 % (c2 0.686 vs 0.720 ms, same c5 time)
+  rc = launch_x(s);
+  if (rc != TF_OK) return rc;
   const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
   if (wide) {
     // border windows (CTA kernel) on a forked stream, concurrently with the wide kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
-    TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
-    TF_CUDA(cudaEventRecord(g.ev_join, side));
+    const bool border_after = std::getenv("TF_GEN_BEFORE") ? false : !graph;  // as in the warp-kernel branch
+    if (!border_after) {
+      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+      TF_CUDA(cudaEventRecord(g.ev_join, side));
+    }
     const int wgrid = g.sms * g.wide_occ[w64][wide];
     const size_t per = static_cast<size_t>(wgrid) * p.iters;  // log entries per band slot
     TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
@@ -591,6 +600,10 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(tfb::fse_wide_launch(wide, w64, w,
                                  static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1))),
                                  wide_smem, s));
+    if (border_after) {
+      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+      TF_CUDA(cudaEventRecord(g.ev_join, side));
+    }
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else if (wbpt) {
     // border windows (CTA kernel) on a forked stream, concurrently with the warp kernel
@@ -601,15 +614,27 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     const size_t per = static_cast<size_t>(wgrid + ggrid) * p.iters;  // log entries per band slot
     TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
     TF_CUDA(g.wlog_c.ensure(nslots * per * sizeof(double2)));
-    if (gbpth) {
-      tfb::FseLaunch ga = a;
-      ga.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
-      ga.wlog_c = g.wlog_c.as<double2>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
-      TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, side));
-    } else {
-      TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+    const auto launch_border = [&]() -> int {
+      if (gbpth) {
+        tfb::FseLaunch ga = a;
+        ga.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
+        ga.wlog_c = g.wlog_c.as<double2>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
+        TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, side));
+      } else {
+        TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+      }
+      TF_CUDA(cudaEventRecord(g.ev_join, side));
+      return TF_OK;
+    };
+    // launch order: the persistent main kernel's CTAs must be dispatched first.  Direct
+    // launches: main first, then the border kernel on the fork (the other order made c2
+    // bimodal, 0.686 / 0.720 ms per process); in a captured graph the opposite capture order
+    // gives that dispatch order (measured: 0.699 vs 0.731 ms per step)
+    const bool border_after = std::getenv("TF_GEN_BEFORE") ? false : !graph;
+    if (!border_after) {
+      rc = launch_border();
+      if (rc != TF_OK) return rc;
     }
-    TF_CUDA(cudaEventRecord(g.ev_join, side));
     tfb::FseLaunch w = a;
     w.blocks = wblocks;
     w.n_blocks = counters + 2;
@@ -627,15 +652,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     } else {
       TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wg, wsmem, s));
     }
+    if (border_after) {
+      rc = launch_border();
+      if (rc != TF_OK) return rc;
+    }
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
   }
-  // the hybrid's EXACT kernel after the FSE kernels, on the launch stream: launched
-  // concurrently (before or after them on a fork) even an empty list cost c2 5-11 % — its
-  // CTAs competed for SM slots with the persistent FSE kernels
-  rc = launch_x(s);
-  if (rc != TF_OK) return rc;
+
   if (ktime) {
     TF_CUDA(cudaStreamSynchronize(s));
     int32_t cnt[tfb::kCounters];
