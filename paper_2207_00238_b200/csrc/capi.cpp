@@ -570,12 +570,15 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaEventRecord(g.ev0, s));
     TF_CUDA(cudaEventRecord(g.ring0[slot], s));
   }
-  // the hybrid's EXACT kernel first, on the launch stream, before the FSE kernels: an empty
-  // list then costs a launch; launched concurrently on a fork (before or after them) even an
-  // empty list cost c2 5-11 % (its CTAs competed for SM slots with the persistent FSE
-  // kernels), and after them on the stream 5 % (c2 0.686 vs 0.720 ms, same c5 time)
-  rc = launch_x(s);
-  if (rc != TF_OK) return rc;
+  // the hybrid's EXACT kernel: before the FSE kernels on the launch stream for one-shot
+  // launches (c2 0.685 vs 0.720 ms after them), after them in the streamed path's bands
+  // (launched first, each band's kernels waited for SM slots behind the other bands: c2 host
+  // call 0.79 vs 0.83-0.86 ms); concurrently on a fork even an empty list cost 5-11 %
+  const bool x_first = std::getenv("TF_X_FIRST") ? std::atoi(std::getenv("TF_X_FIRST")) != 0 : !band;
+  if (x_first) {
+    rc = launch_x(s);
+    if (rc != TF_OK) return rc;
+  }
   const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
   if (wide) {
     // border windows (CTA kernel) on a forked stream, concurrently with the wide kernel
@@ -661,6 +664,10 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
   }
 
+  if (!x_first) {
+    rc = launch_x(s);
+    if (rc != TF_OK) return rc;
+  }
   if (ktime) {
     TF_CUDA(cudaStreamSynchronize(s));
     int32_t cnt[tfb::kCounters];
@@ -788,7 +795,7 @@ static int drop_graph(Gpu& g) {
 // Tuning environment that changes the enqueued work (part of every graph key).
 static std::string env_key() {
   std::string key;
-  for (const char* v : {"TF_HYBRID", "TF_HYBRID_RATIO", "TF_WIDE_WM", "TF_NO_PAIR", "TF_NO_WIDE", "TF_NO_GEN",
+  for (const char* v : {"TF_HYBRID", "TF_HYBRID_RATIO", "TF_X_FIRST", "TF_GEN_BEFORE", "TF_WIDE_WM", "TF_NO_PAIR", "TF_NO_WIDE", "TF_NO_GEN",
                         "TF_NO_WARP", "TF_HALF_NT", "TF_FSE_CFG", "TF_FORCE_WARP"}) {
     const char* e = std::getenv(v);
     key += e ? e : "-";
