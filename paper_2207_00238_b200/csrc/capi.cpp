@@ -956,6 +956,15 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
   if (rc != TF_OK) return rc;
   const int64_t plan_us = us_since(t0);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
+  // a call inside the caller's own stream capture is refused before touching the stream (the
+  // capture stays valid): the enqueue reads pinned staging and device tables that later calls
+  // of another shape overwrite, which a foreign graph replayed later would read stale.  Repeated
+  // identical calls are replayed from the library's own graph below instead.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  TF_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone)
+    return set_error(TF_EINVAL, "stream is capturing a CUDA graph: call tf_tiled_extrapolate_device outside "
+                                "the capture (repeated identical calls replay the library's own graph)");
   if (!stats && !std::getenv("TF_NO_GRAPH")) {
     // graph path: identical repeated calls (the serving / benchmark loop) replay one CUDA
     // graph of the whole enqueue sequence, so the GPU runs it back to back without waiting

@@ -418,3 +418,38 @@ def test_gpu_reproduces_reference_golden_fixtures(ctx, fctx, name):
         dd = np.abs(fa.astype(int) - d["out"].astype(int))[unk]
         assert (dd <= 1).mean() >= FAST_WITHIN1 or dd.size < 1000 and (dd <= 1).mean() >= 0.99, name
     assert np.array_equal(fa[~unk], d["img"][~unk])
+
+
+def test_device_path_refuses_a_caller_capture(fctx):
+    """Called while the caller captures its stream into a CUDA graph, the device path raises
+    ValueError without touching the stream: the caller's capture stays valid, and the next
+    plain call still matches the direct result (repeats replay the library's own graph)."""
+    import torch
+    wl = CONFIGS[2]
+    W, H = 320, 180
+    img, kn = T.synth_frame(2, 5, W, H)
+    want, _ = fctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
+    d_img = torch.from_numpy(img.reshape(-1)).cuda()
+    d_kn = torch.from_numpy(kn.reshape(-1)).cuda()
+    d_out = torch.empty_like(d_img)
+    s = torch.cuda.Stream()
+    call = lambda: fctx.tiled_device(d_img.data_ptr(), d_kn.data_ptr(), d_out.data_ptr(), W, H, 1, wl.tiles,
+                                     wl.overlap, wl.params, stream=s.cuda_stream)
+    with torch.cuda.stream(s):
+        call()
+    torch.cuda.synchronize()
+    x = torch.zeros(16, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        x += 1
+        with pytest.raises(ValueError, match="capturing"):
+            call()
+    g.replay()
+    torch.cuda.synchronize()
+    assert float(x[0]) == 1.0
+    d_out.zero_()
+    with torch.cuda.stream(s):
+        call()
+        call()
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().reshape(H, W), want)
