@@ -102,7 +102,10 @@ typedef struct tf_ctx tf_ctx;
 /* ---- library / context ------------------------------------------------ */
 int tf_abi_version(void);
 /* n_gpus >= 1; device_ids may be NULL (devices 0..n_gpus-1).  Returns NULL on
- * failure (see tf_last_error(NULL)). */
+ * failure (see tf_last_error(NULL)).  A context owns streams, device buffers
+ * and pinned staging and serves one caller at a time: give each worker thread
+ * its own (as each reference worker owns its Extrapolator, runtime.hpp) or
+ * serialise calls on a shared one. */
 tf_ctx* tf_create(int n_gpus, const int* device_ids);
 void tf_destroy(tf_ctx* ctx);
 const char* tf_last_error(const tf_ctx* ctx);
