@@ -150,6 +150,8 @@ struct Gpu {
   int gocc[33] = {};          // FAST border-window (GEN) half kernel occupancy per rows-per-lane
   int gocc_smem[33] = {};
   DevBuf wblocks, wlog_kl, wlog_c;
+  DevBuf big;                                   // big-window kernel scratch (BigLayout per CTA)
+  int big_occ = 0;
   DevBuf dfield0, dfield1, dfoff, dpoff;        // diffusion: FP64 fields, tile offsets
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
   // ring of (start, stop) events around the most recent FSE kernel launches
@@ -317,21 +319,23 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // bins the CTA kernel's threads carry: the full window, or FAST's Hermitian half
   const bool half = tfb::cta_half(exact);
   const int ncarry = half ? (pl.wmax / 2 + 1) * pl.wmax : pl.nmax;
-  const int cfg = tfb::pick_config(ncarry, exact);
-  if (cfg < 0)
-    return set_error(TF_EUNSUPPORTED, "support window of " + std::to_string(pl.nmax) +
-                                          " bins exceeds the kernel capacity (8192)");
+  const int cfg0 = tfb::pick_config(ncarry, exact);
+  const int cfg = cfg0 >= 0 ? cfg0 : 0;
   const int nt = tfb::kCfgs[cfg].nt, nb = nt * tfb::kCfgs[cfg].bpt;
   const tfb::SmemLayout lay(nb, pl.wmax, p.iters, nt / 32, half ? pl.wmax * pl.wmax : nb);
-  if (lay.total > 227 * 1024)
-    return set_error(TF_EUNSUPPORTED, "shared-memory footprint " + std::to_string(lay.total) +
-                                          " B exceeds 227 KB");
-  if (g.occ_smem[exact][cfg] != lay.total) {
+  // windows or selection logs past the shared-memory kernels' capacity: every block of the
+  // launch on the big-window kernel (global scratch; TF_FORCE_BIG=1 forces it, for tests)
+  bool big = cfg0 < 0 || lay.total > 227 * 1024 || std::getenv("TF_FORCE_BIG");
+  if (!big && g.occ_smem[exact][cfg] != lay.total) {
     int occ = 0;
     TF_CUDA(tfb::fse_prepare(cfg, exact, lay.total, &occ));
-    if (occ < 1) return set_error(TF_EUNSUPPORTED, "FSE kernel cannot be resident");
     g.occ[exact][cfg] = occ;
     g.occ_smem[exact][cfg] = lay.total;
+  }
+  if (!big && g.occ[exact][cfg] < 1) big = true;
+  if (big && g.big_occ < 1) {
+    TF_CUDA(tfb::fse_big_prepare(&g.big_occ));
+    if (g.big_occ < 1) return set_error(TF_EUNSUPPORTED, "big-window FSE kernel cannot be resident");
   }
   // warp-per-block kernels for full windows (TF_NO_WARP=1 disables):
   //  EXACT: fse_warp_kernel when 32 % span == 0 and 8 or 16 bins per lane (measured: the
@@ -339,7 +343,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   //  FAST:  fse_half_kernel (Hermitian half spectrum) for span in {8, 16, 32}, one or two
   //         warps per block (TF_HALF_NT=32|64 overrides the per-span default).
   const int span = p.block + 2 * p.margin;
-  const bool nowarp = std::getenv("TF_NO_WARP") || span > pl.wmax;
+  const bool nowarp = std::getenv("TF_NO_WARP") || span > pl.wmax || big;
   int wbpt = 0, wkind = 0;  // 1 = exact warp kernel, 2 = FAST half-spectrum warp kernel
   int hnt = 32;  // threads per block of the half-spectrum kernel (measured: 64 is slower)
   if (const char* e = std::getenv("TF_HALF_NT")) hnt = std::atoi(e);
@@ -430,10 +434,10 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   if (std::getenv("TF_VERBOSE"))
     std::fprintf(stderr,
                  "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d"
-                 " | wide %d smem %d occ %d\n",
+                 " | wide %d smem %d occ %d | big %d\n",
                  nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
                  wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0, wide,
-                 wide_smem, wide ? g.wide_occ[w64][wide] : 0);
+                 wide_smem, wide ? g.wide_occ[w64][wide] : 0, big ? 1 : 0);
   int rc = TF_OK;
   const size_t n_tiles = pl.tiles.size();
   if (bd.first) {
@@ -475,7 +479,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // EXACT kernel for the FAST hybrid's ill-conditioned blocks (full-spectrum CTA kernel)
   int cfgx = -1;
   int xsmem = 0;
-  if (!exact) {
+  if (!exact && !big) {
     cfgx = tfb::pick_config(pl.nmax, true);
     if (cfgx >= 0) {
       const int ntx = tfb::kCfgs[cfgx].nt, nbx = ntx * tfb::kCfgs[cfgx].bpt;
@@ -660,6 +664,17 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       if (rc != TF_OK) return rc;
     }
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
+  } else if (big) {
+    // per-CTA scratch, at most ~4 GB per band slot
+    const tfb::BigLayout bl(pl.nmax, p.iters);
+    int64_t bg = std::min<int64_t>(static_cast<int64_t>(g.sms) * g.big_occ, std::max<int64_t>(cand, 1));
+    bg = std::max<int64_t>(1, std::min<int64_t>(bg, (int64_t{4} << 30) / static_cast<int64_t>(bl.total)));
+    const size_t per = static_cast<size_t>(bg) * bl.total;
+    TF_CUDA(g.big.ensure(nslots * per));
+    tfb::FseLaunch b = a;
+    b.scratch = g.big.as<unsigned char>() + bslot * per;
+    b.nmax = pl.nmax;
+    TF_CUDA(tfb::fse_big_launch(b, static_cast<int>(bg), s));
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
   }
@@ -796,7 +811,7 @@ static int drop_graph(Gpu& g) {
 static std::string env_key() {
   std::string key;
   for (const char* v : {"TF_HYBRID", "TF_HYBRID_RATIO", "TF_X_FIRST", "TF_GEN_BEFORE", "TF_WIDE_WM", "TF_NO_PAIR", "TF_NO_WIDE", "TF_NO_GEN",
-                        "TF_NO_WARP", "TF_HALF_NT", "TF_FSE_CFG", "TF_FORCE_WARP"}) {
+                        "TF_NO_WARP", "TF_HALF_NT", "TF_FSE_CFG", "TF_FORCE_WARP", "TF_FORCE_BIG"}) {
     const char* e = std::getenv(v);
     key += e ? e : "-";
     key += '|';
@@ -891,7 +906,8 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.ev_cout) cudaEventDestroy(g.ev_cout);
     for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
                       &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv, &g.wblocks,
-                      &g.wlog_kl, &g.wlog_c, &g.qbuf})
+                      &g.wlog_kl, &g.wlog_c, &g.qbuf, &g.xblocks, &g.big, &g.dfield0, &g.dfield1,
+                      &g.dfoff, &g.dpoff})
       b->release();
     if (g.pinned) cudaFreeHost(g.pinned);
     for (int r = 0; r < Gpu::kRing; ++r) {

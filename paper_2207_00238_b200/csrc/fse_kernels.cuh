@@ -51,7 +51,34 @@ struct FseLaunch {
   BlockStat* stats;       // optional
   int32_t* wlog_kl;       // warp kernel: per-CTA selection log scratch (iters entries each)
   double2* wlog_c;
+  unsigned char* scratch;  // big-window kernel: per-CTA spectra and model (BigLayout bytes each)
+  int32_t nmax;            // big-window kernel: largest support window (bins) of the launch
 };
+
+// Big-window kernel (windows past the shared-memory kernels' capacity, or selection logs too
+// long for shared memory): per-CTA global scratch, 16-byte aligned sections
+//   [W: N double2][R: N double2][row pass of w: N double2][of w*v: N double2]
+//   [(w, w*v): N double2][first-touch positions: N int32][touched list: 2I int32]
+//   [model values: 2I double2][selection log: I int32 + I double2]
+struct BigLayout {
+  size_t off_w, off_r, off_rw, off_rr, off_cw, off_post, off_lst, off_mval, off_logkl, off_logc, total;
+  __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+  __host__ __device__ BigLayout(int nmax, int iters) {
+    const size_t n = static_cast<size_t>(nmax), it = static_cast<size_t>(iters);
+    off_w = 0;
+    off_r = off_w + 16 * n;
+    off_rw = off_r + 16 * n;
+    off_rr = off_rw + 16 * n;
+    off_cw = off_rr + 16 * n;
+    off_post = off_cw + 16 * n;
+    off_lst = al(off_post + 4 * n);
+    off_mval = al(off_lst + 8 * it);
+    off_logkl = off_mval + 32 * it;
+    off_logc = al(off_logkl + 4 * it);
+    total = al(off_logc + 16 * it);
+  }
+};
+constexpr int kBigThreads = 512;
 
 struct EnumLaunch {
   const uint8_t* known;
@@ -244,6 +271,8 @@ constexpr int kNumCfgs = 10;
 extern const KernelCfg kCfgs[kNumCfgs];
 int pick_config(int nmax, bool exact);  // smallest config holding nmax bins, -1 if none
 cudaError_t fse_prepare(int cfg, bool exact, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_big_prepare(int* ctas_per_sm);
+cudaError_t fse_big_launch(const FseLaunch& a, int grid, cudaStream_t s);
 cudaError_t fse_launch(int cfg, bool exact, const FseLaunch& a, int grid, int smem_bytes,
                        cudaStream_t s);
 // Diffusion extrapolator over the tiles' halos (diffusion.cu).  foff: FP64 field offset of

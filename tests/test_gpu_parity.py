@@ -453,3 +453,40 @@ def test_device_path_refuses_a_caller_capture(fctx):
         call()
     torch.cuda.synchronize()
     assert np.array_equal(d_out.cpu().numpy().reshape(H, W), want)
+
+
+def test_big_window_kernel_forced_on_small_cases(ctx, fctx, monkeypatch):
+    """The global-scratch big-window kernel, forced onto ordinary launches (TF_FORCE_BIG=1):
+    byte-identical to the oracle in both modes (it computes with EXACT arithmetic)."""
+    monkeypatch.setenv("TF_FORCE_BIG", "1")
+    rng = np.random.default_rng(77)
+    for trial in range(16):
+        w, h = int(rng.integers(6, 80)), int(rng.integers(6, 80))
+        B, m, I = int(rng.integers(2, 17)), int(rng.integers(0, 20)), int(rng.integers(1, 60))
+        g, r = float(rng.uniform(0.05, 1.0)), float(rng.uniform(0.2, 0.95))
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        kn = (rng.random((h, w)) > rng.uniform(0.05, 0.7)).astype(np.uint8)
+        tiles = int(rng.integers(1, 4))
+        p = _params(B, m, I, g, r)
+        try:
+            want, bpt = O.tiled(img, kn, tiles, 3, B, m, I, g, r)
+        except O.OracleError:
+            continue
+        for c in (ctx, fctx):
+            got, st = c.tiled(img, kn, tiles, 3, p)
+            assert np.array_equal(got, want), f"trial {trial} {c.mode}: {(got != want).sum()} px differ"
+            assert st.blocks_reference == int(bpt.sum())
+
+
+@pytest.mark.parametrize("B,m,I,W,H", [(32, 32, 25, 160, 128),    # 96x96 windows: 9216 bins
+                                       (64, 64, 60, 320, 256),    # 192x192 windows: 36864 bins
+                                       (8, 12, 12000, 48, 40)])   # 32x32 windows, 12000-entry logs
+def test_big_windows_and_long_logs_equal_oracle(ctx, fctx, B, m, I, W, H):
+    """Support windows and selection logs past the shared-memory kernels' capacity (formerly
+    TF_EUNSUPPORTED) run on the big-window kernel: byte-identical to the oracle in both modes."""
+    img, kn = T.synth_frame(1, 3, W, H)
+    want = O.fse_lite(img, kn, B, m, I, 0.5, 0.8)
+    for c in (ctx, fctx):
+        got, st = c.tiled(img, kn, 1, 0, _params(B, m, I, 0.5, 0.8))
+        assert np.array_equal(got, want), f"{c.mode}: {(got != want).sum()} px differ"
+        assert st.blocks_processed == st.blocks_reference == T.count_blocks(kn, B)
