@@ -490,3 +490,20 @@ def test_big_windows_and_long_logs_equal_oracle(ctx, fctx, B, m, I, W, H):
         got, st = c.tiled(img, kn, 1, 0, _params(B, m, I, 0.5, 0.8))
         assert np.array_equal(got, want), f"{c.mode}: {(got != want).sum()} px differ"
         assert st.blocks_processed == st.blocks_reference == T.count_blocks(kn, B)
+
+
+def test_degenerate_shapes_equal_oracle(ctx, fctx):
+    """1x1, single-row and single-column images, blocks larger than the image, margin 0:
+    EXACT byte-identical to the oracle, FAST within +-1 of it on every pixel."""
+    rng = np.random.default_rng(9)
+    shapes = [(1, 1), (1, 7), (7, 1), (2, 2), (3, 5), (5, 3), (1, 40), (40, 1)]
+    for (w, h) in shapes:
+        for (B, m) in [(2, 0), (4, 8), (16, 3)]:
+            img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+            kn = (rng.random((h, w)) > 0.5).astype(np.uint8)
+            want = O.fse_lite(img, kn, B, m, 20, 0.5, 0.8)
+            got, st = ctx.tiled(img, kn, 1, 0, _params(B, m, 20, 0.5, 0.8))
+            assert np.array_equal(got, want), f"{w}x{h} B={B} m={m}"
+            assert st.blocks_reference == T.count_blocks(kn, B)
+            fgot, _ = fctx.tiled(img, kn, 1, 0, _params(B, m, 20, 0.5, 0.8))
+            assert np.abs(fgot.astype(int) - want.astype(int)).max() <= 1, f"fast {w}x{h} B={B} m={m}"
