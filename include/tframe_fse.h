@@ -52,8 +52,9 @@ typedef enum tf_status {
   TF_ECUDA = 5,        /* CUDA runtime failure / no sm_100 device         */
   TF_ENCCL = 6,        /* NCCL failure                                    */
   TF_ENOMEM = 7,       /* host or device allocation failure               */
-  TF_EUNSUPPORTED = 8  /* beyond the device path's index ranges (> 65535
-                          blocks along a halo axis, > 2^31 blocks a call) */
+  TF_EUNSUPPORTED = 8  /* beyond the device path's index ranges (window
+                          side > 2048, > 65535 blocks along a halo axis,
+                          > 2^31 blocks a call)                           */
 } tf_status;
 
 /* Arithmetic mode of the FSE kernel. */

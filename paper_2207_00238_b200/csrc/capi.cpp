@@ -319,6 +319,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // bins the CTA kernel's threads carry: the full window, or FAST's Hermitian half
   const bool half = tfb::cta_half(exact);
   const int ncarry = half ? (pl.wmax / 2 + 1) * pl.wmax : pl.nmax;
+  if (pl.wmax > 2048)  // index arithmetic (k*x mod M through a float reciprocal) holds to 2^22
+    return set_error(TF_EUNSUPPORTED, "support window side " + std::to_string(pl.wmax) + " exceeds 2048");
   const int cfg0 = tfb::pick_config(ncarry, exact);
   const int cfg = cfg0 >= 0 ? cfg0 : 0;
   const int nt = tfb::kCfgs[cfg].nt, nb = nt * tfb::kCfgs[cfg].bpt;
