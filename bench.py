@@ -1,36 +1,45 @@
 #!/usr/bin/env python
 """Benchmark of the B200 FSE-lite hot path (BASELINE.json metric: reconstructed Mpixel/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode exact|fast]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode fast|exact] [--config 1..5]
 
-Workload = BASELINE configs[1] (= SURVEY config c2): one 1920x1080 u8 frame,
-8x8 aligned cell loss p=0.10, FSE block 8 / border 12 (32x32 window = DFT),
-200 iterations, rho 0.8, gamma 0.5, tiled into 4 overlapping tiles (d = 12).
-A "step" is one pass of the hot path over one frame per GPU.
+Workload (default) = BASELINE config c3, the one the "1/2/4/8 B200" sweep is defined on:
+one 3840x2160 u8 frame, i.i.d. pixel loss p = 0.20, FSE block 4 / border 6 (16x16 window
+= DFT), 50 iterations, rho 0.7, gamma 0.5, proposed tiling into 8 overlapping tiles, d = 6.
+The tiling is FIXED at 8 tiles for every GPU count, so the output is identical across N
+(strong scaling).  A "step" is one pass of the hot path over that frame.
 
-N > 1 (torchrun, one process per GPU): every rank reconstructs its own frame
-(per-rank seed) and the frames are gathered to rank 0 with NCCL over NVLink
-(weak scaling; the gather is inside the timed region).
+N > 1 (torchrun, one process per GPU): rank r reconstructs the tiles it owns (LPT
+assignment of the 8 tiles over N ranks, tf_tiled_extrapolate_device part=r, n_parts=N) and
+the core rectangles are gathered to rank 0 with NCCL send/recv over NVLink
+(tf_comm_gather_cores) inside the timed region; max over ranks.
 
-value  : device path, inputs resident in HBM (tf_tiled_extrapolate_device),
-         L2 flushed between steps (a 256 MiB write outside the timed events), in the
-         headline mode (default FAST: FMA + Hermitian half spectrum, within the north-star
-         tolerance, checked on this very frame and reported under "parity"); the EXACT
-         mode (byte-identical to the reference, also checked here) is timed and reported.
-e2e    : the same through the public host-buffer call (tf_tiled_extrapolate on pinned
-         HOST buffers): H2D of image + mask, FSE, D2H of the result inside the call
-         (streamed in row bands so copies overlap the kernels), every rank its own frame.
-roofline: FP64-bound kernels; achieved = executed FP64 flops per launch (== the
-         SURVEY §8(d) algorithmic sum_b F_b in EXACT mode) / mean FSE time (CUDA events
-         on the launch stream), peak = FP64 DFMA rate measured live (tf_calibrate).
---impl reference: the reference CPU FSE (oracle/_ref: the unmodified tframe
-         headers compiled by oracle/Makefile), all host threads, same frame.
+value  : device path, inputs resident in HBM, L2 flushed between steps (256 MiB write
+         outside the timed events), CUDA events on the launch stream, max over ranks.
+         Headline mode FAST: binary64 with FMA contraction on the Hermitian half spectrum
+         (within the north-star tolerance, checked on this very frame under "parity").
+         EXACT (byte-identical to the reference) is timed and reported beside it.
+e2e    : the same through the public host-buffer call: N = 1 tf_tiled_extrapolate (pinned
+         HOST buffers, H2D + FSE + D2H inside the call, streamed in row bands); N > 1
+         tf_tiled_extrapolate_rank (H2D of the rank's own halo rectangles, FSE, NCCL core
+         gather, D2H of the frame on rank 0).
+roofline: FP64-bound kernels.  SURVEY §8(d): achieved = sum_b F_b / t_kernel when the
+         kernels execute >= 0.9 sum_b F_b, else (FAST's half spectrum) the FP64 flops the
+         kernels execute (ncu: 2 x DFMA + DADD + DMUL thread instructions, the committed
+         profiles/ capture of this workload) / t_kernel.  peak = the FP64 pipe's measured
+         maximum on this GPU (DMMA m8n8k4 rate, tf_calibrate_peaks; DFMA reported beside).
+--impl reference: the reference CPU FSE (oracle/_ref: the unmodified tframe headers
+         compiled by oracle/Makefile) on all host threads; its inputs come from the same
+         generator compiled into that library (no product library is loaded).  Each step
+         is a bounded sample: one of the 8 tiles (the core it owns, round robin).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -43,8 +52,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG = 2  # BASELINE configs[1]
+CONFIG = 3  # BASELINE configs[2]: the config BASELINE's 1/2/4/8-GPU sweep is quoted on
 METRIC = "reconstructed Mpixel/s (FSE, 1/2/4/8 B200) and % of FLOP roofline vs CPU ref"
+L2_NOTE = "GPU arm: L2 flushed between steps (256 MiB write outside the timed events)"
 
 
 def _env_int(k, d):
@@ -52,6 +62,18 @@ def _env_int(k, d):
         return int(os.environ.get(k, d))
     except ValueError:
         return d
+
+
+def host_info() -> dict:
+    model = platform.processor() or ""
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
 
 
 class ClockSampler:
@@ -99,69 +121,95 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_frames(wl, frame):
-    from paper_2207_00238_b200 import tframe as T
-    return T.synth_frame(wl.config, frame, wl.W, wl.H)
+def config_of(wl, world) -> dict:
+    """The `config` object of both arms (identical keys and values for the same run)."""
+    return {"workload": wl.describe(), "frames": wl.frames, "tiles": wl.tiles, "overlap": wl.overlap,
+            "parallelism": (f"{wl.tiles} fixed tiles over {world} GPUs (LPT), NCCL core gather to rank 0"
+                            if world > 1 else f"{wl.tiles} fixed tiles on one GPU"),
+            "l2": L2_NOTE}
 
 
-def cpu_reference(wl, img, kn, steps, warmup, threads=None):
-    """The reference's own FSE (oracle/_ref, unmodified tframe headers), bit-exact
-    band split over all host threads.  Returns (Mpix/s, out, info)."""
+def ref_frames(wl):
+    """Inputs for the CPU arms: the versioned generator compiled into oracle/_ref."""
     import oracle as O
+    imgs, kns = zip(*[O.ref_synth_frame(wl.config, f, wl.W, wl.H) for f in range(wl.frames)])
+    return np.stack(imgs), np.stack(kns)
+
+
+def ref_args(wl):
     p = wl.params
-    threads = threads or os.cpu_count() or 1
-    args = (wl.tiles, wl.overlap, p.block_size, p.support_margin, p.model_iterations,
+    return (wl.tiles, wl.overlap, p.block_size, p.support_margin, p.model_iterations,
             p.compensation, p.weight_decay)
-    out = None
-    for _ in range(warmup):
-        out = O.ref_tiled_allcores(img, kn, *args, threads=threads)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        out = O.ref_tiled_allcores(img, kn, *args, threads=threads)
-        times.append(time.perf_counter() - t0)
-    mean = sum(times) / len(times)
-    return wl.W * wl.H / mean / 1e6, out, {"threads": threads, "s_per_frame": mean}
+
+
+def core_pixels(wl, part, n_parts):
+    from paper_2207_00238_b200.tframe import plan_proposed  # pure host tiling (no GPU)
+    cores = plan_proposed(wl.W, wl.H, wl.tiles)
+    return sum(c[2] * c[3] for t, c in enumerate(cores) if t % n_parts == part) * wl.frames
+
+
+def ref_core_pixels(wl, part, n_parts):
+    import oracle as O
+    cores = O.ref_plan_proposed(wl.W, wl.H, wl.tiles)
+    return sum(int(c[2]) * int(c[3]) for t, c in enumerate(cores) if t % n_parts == part) * wl.frames
 
 
 def run_reference(args, wl, rank, world):
+    """--impl reference: the reference's FSE-lite on all host threads, rank 0 only."""
     if rank != 0:
         return
-    from paper_2207_00238_b200 import tframe as T  # noqa: F401  (synthetic generator only)
     import oracle as O
     if not O.have_ref():
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libtframe_ref.so not built (needs /root/reference at build time)"}))
         return
-    img, kn = make_frames(wl, 0)
-    steps, warmup = max(1, args.steps), max(0, min(args.warmup, 1))
-    v, _, info = cpu_reference(wl, img, kn, steps, warmup)
+    img, kn = ref_frames(wl)
+    threads = os.cpu_count() or 1
+    n_sample = wl.tiles if wl.tiles > 1 else 1
+    warmup = max(3, args.warmup)
+    times, pix = [], 0
+    out = img.copy()
+    for i in range(warmup + args.steps):
+        part = i % n_sample
+        t0 = time.perf_counter()
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, out=out, part=part, n_parts=n_sample)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+            pix += ref_core_pixels(wl, part, n_sample)
+    tot = sum(times)
+    v = pix / tot / 1e6
+    host = host_info()
+    sample = (f"each step one of the {n_sample} tiles of the c{wl.config} frame(s) (its core, round robin), "
+              f"reference fse_lite_extrapolate via the bit-exact B-aligned band split on {threads} threads")
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "Mpixel/s",
-        "n_gpus": world, "steps": steps, "warmup": warmup,
-        "ms_per_step": round(info["s_per_frame"] * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.describe(), "frames_per_step": 1},
-        "cpu_baseline": {"value": round(v, 3), "unit": "Mpixel/s", "cores": info["threads"],
-                         "kind": "reference",
-                         "sample": f"full c{wl.config} frame per step ({wl.W}x{wl.H}, {wl.tiles} tiles, d={wl.overlap}), "
-                                   "bit-exact B-aligned band split over all host threads"},
-        "e2e": {"value": round(v, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "Mpixel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": warmup,
+        "ms_per_step": round(tot / len(times) * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (versioned generator v1, seeds 1000*{wl.config}+frame)",
+        "config": config_of(wl, world),
+        "cpu_baseline": {"value": round(v, 4), "unit": "Mpixel/s", "cores": threads, "kind": "reference",
+                         "sample": sample, **host},
+        "e2e": {"value": round(v, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    loaded = [ln.split()[-1] for ln in open("/proc/self/maps") if ln.rstrip().endswith(".so")]
+    line["native_libraries"] = sorted({Path(p).name for p in loaded if "tframe" in p})
+    assert "libtframe_b200.so" not in line["native_libraries"], "reference arm loaded the product library"
     print(json.dumps(line), flush=True)
 
 
-def ncu_profile(mode, config=CONFIG):
-    """DRAM bytes (read + write) per launch of the FSE kernels and their shared-memory
-    wavefront utilisation, from the committed `ncu --set full` summary of this workload
-    (profiles/rNN_ncu_fse_c2_<mode>_summary.csv, written by tools/ncu_summary.py)."""
+def ncu_profile(mode, config):
+    """FP64 flops, DRAM bytes and pipe utilisation per launch of the FSE kernels from the
+    committed `ncu --set full` summary of this workload (profiles/rNN_ncu_*_c<config>_<mode>_summary.csv,
+    written by tools/ncu_summary.py; the newest round wins)."""
     import csv
     import glob
     files = sorted(glob.glob(str(ROOT / "profiles" / f"r*_ncu_*_c{config}_{mode}_summary.csv")))
     if not files:
         return {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    traffic, smem, found, fp64, pipe = 0.0, [], False, None, []
+    traffic, smem, fp64, pipe, found = 0.0, [], 0.0, [], False
     with open(files[-1]) as f:
         rows = list(csv.DictReader(f))
     for r in rows:
@@ -173,13 +221,13 @@ def ncu_profile(mode, config=CONFIG):
         if r["metric"] == "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed":
             smem.append(round(float(r["value"]), 1))
         if r["metric"] == "derived_fp64_flops":
-            fp64 = (fp64 or 0.0) + float(r["value"])
+            fp64 += float(r["value"])
         if r["metric"] == "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active":
             pipe.append(round(float(r["value"]), 1))
     if not found:
         return {}
-    return {"traffic": int(traffic), "smem_pct": smem, "source": Path(files[-1]).name,
-            "fp64_flops": fp64, "fp64_pipe_pct": pipe}
+    return {"traffic": int(traffic), "smem_pct": smem, "source": "profiles/" + Path(files[-1]).name,
+            "fp64_flops": fp64 or None, "fp64_pipe_pct": pipe}
 
 
 def main():
@@ -192,8 +240,8 @@ def main():
                     help="headline arithmetic mode; the other mode is timed and reported too")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", type=int, default=CONFIG, choices=[1, 2, 3, 4, 5],
-                    help="BASELINE config (default 2, the one the metric is quoted on; the others "
-                         "for the per-config evidence in profiles/)")
+                    help="BASELINE config (default 3: the 1/2/4/8-GPU sweep's config); the others "
+                         "for the per-config evidence in profiles/")
     args = ap.parse_args()
 
     rank = _env_int("RANK", 0)
@@ -207,12 +255,13 @@ def main():
         run_reference(args, wl, rank, world)
         return
 
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
     from paper_2207_00238_b200 import _native as N
     from paper_2207_00238_b200 import tframe as T
-    import ctypes as C
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -232,34 +281,41 @@ def main():
         uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
         N.check(L.tf_comm_init(ctx.handle, world, rank, uid))
 
-    # ---- inputs: this rank's frame (seeded per rank), pinned host + HBM copies
-    img_np, kn_np = make_frames(wl, rank)
-    H, W = img_np.shape
-    fb = W * H
+    # ---- inputs: the workload's frame(s), identical on every rank; pinned host + HBM copies
+    frames = [T.synth_frame(wl.config, f, wl.W, wl.H) for f in range(wl.frames)]
+    img_np = np.stack([a for a, _ in frames])
+    kn_np = np.stack([b for _, b in frames])
+    F, H, W = img_np.shape
+    fb = F * W * H
     h_img = torch.from_numpy(img_np.reshape(-1)).pin_memory()
     h_kn = torch.from_numpy(kn_np.reshape(-1)).pin_memory()
     d_img = h_img.to(dev)
     d_kn = h_kn.to(dev)
     d_out = torch.empty_like(d_img)
-    d_all = torch.empty(world * fb, dtype=torch.uint8, device=dev) if (world > 1 and rank == 0) else None
     h_res = torch.empty(fb, dtype=torch.uint8).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     p = wl.params._c()
 
     def device_step():
-        N.check(L.tf_tiled_extrapolate_device(ctx.handle, 0, d_img.data_ptr(), d_kn.data_ptr(), W, H, 1,
-                                              wl.tiles, wl.overlap, C.byref(p), 0, 1, d_out.data_ptr(),
-                                              sptr, None))
+        N.check(L.tf_tiled_extrapolate_device(ctx.handle, 0, d_img.data_ptr(), d_kn.data_ptr(), W, H, F,
+                                              wl.tiles, wl.overlap, C.byref(p), rank, world,
+                                              d_out.data_ptr(), sptr, None))
         if world > 1:
-            N.check(L.tf_comm_gather(ctx.handle, d_out.data_ptr(),
-                                     d_all.data_ptr() if d_all is not None else None, fb, 0, sptr))
+            N.check(L.tf_comm_gather_cores(ctx.handle, d_out.data_ptr(), W, H, F, wl.tiles, 0, sptr))
+
+    e2e_io = {}
 
     def e2e_step():
-        # the call a user makes: tf_tiled_extrapolate on pinned HOST buffers (the library
-        # streams row bands: H2D, FSE and D2H overlap inside the call); every rank
-        # reconstructs its own frame into its own host memory
-        N.check(L.tf_tiled_extrapolate(ctx.handle, h_img.data_ptr(), h_kn.data_ptr(), W, H, 1, wl.tiles,
-                                       wl.overlap, C.byref(p), h_res.data_ptr(), None))
+        # the call a user makes, on pinned HOST buffers: copies inside the call
+        if world == 1:
+            N.check(L.tf_tiled_extrapolate(ctx.handle, h_img.data_ptr(), h_kn.data_ptr(), W, H, F, wl.tiles,
+                                           wl.overlap, C.byref(p), h_res.data_ptr(), None))
+        else:
+            io = (C.c_int64 * 2)()
+            N.check(L.tf_tiled_extrapolate_rank(ctx.handle, h_img.data_ptr(), h_kn.data_ptr(), W, H, F,
+                                                wl.tiles, wl.overlap, C.byref(p), 0,
+                                                h_res.data_ptr() if rank == 0 else None, io))
+            e2e_io["h2d"], e2e_io["d2h"] = io[0], io[1]
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -288,132 +344,182 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def launches():
+        n = C.c_int64(0)
+        N.check(L.tf_kernel_launches(ctx.handle, 0, C.byref(n)))
+        return n.value
+
     other = "exact" if args.mode == "fast" else "fast"
+    warmup = max(3, args.warmup)
 
     def run_mode(mode):
         """Warm up + time the device path in `mode`; returns timing, kernel times, stats, output."""
         ctx.set_mode(mode)
-        for _ in range(max(3, args.warmup)):
+        for _ in range(warmup):
             device_step()
         barrier()
-        out = d_out.cpu().numpy().reshape(H, W).copy()
-        assert np.array_equal(out[kn_np != 0], img_np[kn_np != 0]), "known pixels not preserved"
+        out = d_out.cpu().numpy().reshape(F, H, W).copy()
+        if rank == 0:
+            assert np.array_equal(out[kn_np != 0], img_np[kn_np != 0]), "known pixels not preserved"
+        n0 = launches()
         with ClockSampler(local) as clk:
             ms = timed(device_step, args.steps)
+        nl = launches() - n0
         kt = (C.c_float * args.steps)()
         nk = L.tf_fse_kernel_times(ctx.handle, 0, kt, args.steps)
-        st = ctx.tiled_device(d_img.data_ptr(), d_kn.data_ptr(), d_out.data_ptr(), W, H, 1, wl.tiles,
-                              wl.overlap, wl.params, stream=sptr, want_stats=True)
+        st = ctx.tiled_device(d_img.data_ptr(), d_kn.data_ptr(), d_out.data_ptr(), W, H, F, wl.tiles,
+                              wl.overlap, wl.params, stream=sptr, want_stats=True, part=rank, n_parts=world)
         fse = [kt[i] for i in range(max(nk, 0))]
         return {"ms_step": ms / args.steps, "fse_ms": sum(fse) / len(fse) if fse else st.kernel_ms,
-                "stats": st, "out": out, "clocks": clk.summary()}
+                "stats": st, "out": out, "clocks": clk.summary(), "launches": nl}
 
     res_other = run_mode(other)
     res = run_mode(args.mode)  # headline mode last: the context stays in it for e2e
     ms_step = res["ms_step"]
-    value = world * fb / (ms_step * 1e-3) / 1e6
+    value = fb / (ms_step * 1e-3) / 1e6
 
     # ---- e2e through the C-ABI with host buffers (headline mode)
     for _ in range(2):
         e2e_step()
     ms_e2e = timed(e2e_step, args.steps, host_api=True) / args.steps
-    e2e = world * fb / (ms_e2e * 1e-3) / 1e6
+    e2e = fb / (ms_e2e * 1e-3) / 1e6
+    if world == 1:
+        h2d, d2h = 2 * fb, fb
+    else:
+        t = torch.tensor([e2e_io["h2d"], e2e_io["d2h"]], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        h2d, d2h = int(t[0]), int(t[1])
+    if rank == 0:
+        e2e_out = h_res.numpy().reshape(F, H, W)
+        assert np.array_equal(e2e_out, res["out"]), "host-buffer call differs from the device path"
 
-    # ---- roofline of the headline FSE launch: executed FP64 flops (== the algorithmic
-    # sum_b F_b for EXACT; the FAST half-spectrum kernel executes ~1/3 of it, SURVEY §8(d)
-    # says to use executed flops then) / mean FSE kernel time; peak = live DFMA calibration
-    fp64 = C.c_double(0)
-    smem = C.c_double(0)
-    N.check(L.tf_calibrate(local, C.byref(fp64), C.byref(smem)))
+    # ---- roofline of the headline FSE launch (SURVEY §8(d))
+    dfma, dmma, smem = C.c_double(0), C.c_double(0), C.c_double(0)
+    N.check(L.tf_calibrate_peaks(local, C.byref(dfma), C.byref(dmma), C.byref(smem)))
+    peak = max(dfma.value, dmma.value)
     st = res["stats"]
     mean_k = res["fse_ms"]
-    achieved = st.flops_executed / (mean_k * 1e-3) / 1e12
-    prof = ncu_profile(args.mode, args.config)
-    roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64.value, 3),
-            "unit": "TFLOP/s", "frac": round(achieved / fp64.value, 4),
-            "traffic": prof.get("traffic"),
+    prof = ncu_profile(args.mode, args.config) if world == 1 else {}
+    alg = st.flops
+    if st.flops_executed >= 0.9 * alg:
+        flops, how = alg, "sum_b F_b (SURVEY §8(d)); the kernels execute >= 0.9 of it"
+    elif prof.get("fp64_flops"):
+        flops, how = prof["fp64_flops"], (f"ncu-executed FP64 flops of this launch (2 DFMA + DADD + DMUL thread "
+                                          f"instructions, {prof['source']}): executed < 0.9 sum_b F_b (half spectrum)")
+    else:
+        flops, how = st.flops_executed, "kernel's own executed-FP64 count (no ncu capture of this workload committed)"
+    achieved = flops / (mean_k * 1e-3) / 1e12
+    roof = {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": prof.get("traffic"),
+            "formula": "frac = flops_per_launch / (fse_kernel_ms * 1e-3) / (peak * 1e12)",
+            "flops_per_launch": flops, "flops_source": how,
+            "fse_kernel_ms": round(mean_k, 4),
+            "peak_source": ("max(DMMA m8n8k4, DFMA) rate measured live by tf_calibrate_peaks "
+                            "(MEASURED_PEAKS.json has no FP64 figure)"),
+            "peak_dfma_tflops": round(dfma.value, 3), "peak_dmma_tflops": round(dmma.value, 3),
+            "flops_algorithmic_per_launch": alg, "flops_executed_model_per_launch": st.flops_executed,
+            "algorithmic_tflops": round(alg / (mean_k * 1e-3) / 1e12, 3),
             "traffic_source": prof.get("source"),
             "smem_wavefront_pct_of_peak_ncu": prof.get("smem_pct"),
-            # FP64-only view from the committed ncu capture: FP64 flops the FSE kernels
-            # executed (packed FP32 excluded) over this run's FSE time, and the FP64 pipe's
-            # utilisation per kernel — the kernels are latency/issue-bound, not FP64-pipe-bound
-            "ncu_fp64_flops_per_launch": prof.get("fp64_flops"),
-            "ncu_fp64_tflops": (round(prof["fp64_flops"] / (mean_k * 1e-3) / 1e12, 3)
-                                if prof.get("fp64_flops") else None),
             "fp64_pipe_pct_of_peak_ncu": prof.get("fp64_pipe_pct"),
-            "peak_source": "FP64 DFMA rate measured live by tf_calibrate (MEASURED_PEAKS.json has no FP64 figure)",
-            "fse_kernel_ms": round(mean_k, 4), "flops_executed_per_launch": st.flops_executed,
-            "flops_algorithmic_per_launch": st.flops,
-            "algorithmic_tflops": round(st.flops / (mean_k * 1e-3) / 1e12, 3),
             "smem_peak_tbs": round(smem.value, 2),
             "kernel_share_of_step": round(mean_k / ms_step, 3)}
 
-    # ---- parity of this run: FAST vs EXACT (north-star tolerance), EXACT vs the reference
-    ex_out = res["out"] if args.mode == "exact" else res_other["out"]
-    fa_out = res["out"] if args.mode == "fast" else res_other["out"]
-    unk = kn_np == 0
-    dd = np.abs(ex_out.astype(int) - fa_out.astype(int))[unk]
-
-    # PSNR / SSIM against the ground truth on the GPU (tf_quality: bit-identical to metrics.hpp)
-    qe, qf = ctx.quality(np.stack([img_np, img_np]), np.stack([ex_out, fa_out]), np.stack([kn_np, kn_np]))
-
-    parity = {"fast_within1_of_exact": round(float((dd <= 1).mean()), 6),
-              "fast_max_abs_diff": int(dd.max()) if dd.size else 0,
-              "psnr_exact_db": round(qe["psnr"], 4), "psnr_fast_db": round(qf["psnr"], 4),
-              "ssim_exact": round(qe["ssim"], 6), "ssim_fast": round(qf["ssim"], 6),
-              "psnr_missing_exact_db": round(qe["psnr_missing"], 4),
-              "psnr_missing_fast_db": round(qf["psnr_missing"], 4),
-              "metrics_source": "GPU tf_quality (metrics.hpp restated)",
-              "tolerance": ">= 0.999 within +-1 and |dPSNR| <= 0.05 dB (north star)"}
-    parity["fast_dpsnr_db"] = round(abs(parity["psnr_exact_db"] - parity["psnr_fast_db"]), 5)
-    parity["fast_within_tolerance"] = bool(parity["fast_within1_of_exact"] >= 0.999 and parity["fast_dpsnr_db"] <= 0.05)
-
+    # ---- parity of this run (rank 0 holds the gathered frame): FAST vs EXACT
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
-        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (versioned generator v1, per-rank seed 1000*{wl.config}+rank)",
-        "config": {"workload": wl.describe(), "frames_per_gpu_per_step": 1, "mode": args.mode,
-                   "l2": "flushed between steps (256 MiB write outside the timed events)",
-                   "parallelism": f"dp{world} frames, NCCL gather to rank 0" if world > 1 else "single GPU",
-                   "blocks_processed": st.blocks_processed, "blocks_reference": st.blocks_reference},
+        "steps": args.steps, "warmup": warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (versioned generator v1, seeds 1000*{wl.config}+frame)",
+        "config": config_of(wl, world),
+        "mode": args.mode,
         "e2e": {"value": round(e2e, 3), "unit": "Mpixel/s", "ms_per_step": round(ms_e2e, 4),
-                "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb,
-                "path": "tf_tiled_extrapolate (host buffers, streamed row bands), per rank"},
-        # per step, FAST: enumerate + half-spectrum FSE + border-window (GEN) FSE + the hybrid's
-        # EXACT kernel (empty list on c2); EXACT: enumerate + CTA FSE
-        "gpu_launches": args.steps * (4 if args.mode == "fast" else 2),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": ("tf_tiled_extrapolate (host buffers, streamed row bands)" if world == 1 else
+                         "tf_tiled_extrapolate_rank per rank (own halo rectangles H2D, NCCL core gather, "
+                         "rank-0 D2H)")},
+        "gpu_launches": res["launches"],
         "roofline": roof,
         "clocks": res["clocks"],
-        other + "_mode": {"value": round(world * fb / (res_other["ms_step"] * 1e-3) / 1e6, 3),
+        other + "_mode": {"value": round(fb / (res_other["ms_step"] * 1e-3) / 1e6, 3),
                           "ms_per_step": round(res_other["ms_step"], 4),
                           "fse_kernel_ms": round(res_other["fse_ms"], 4)},
-        "parity": parity,
+        "blocks_processed": st.blocks_processed, "blocks_reference": st.blocks_reference,
     }
-
-    # ---- CPU baseline: rank 0, N = 1 only, the reference on the host cores
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            import oracle as O
-            if O.have_ref():
-                v, ref_out, info = cpu_reference(wl, img_np, kn_np, 1, 0)
-                line["cpu_baseline"] = {
-                    "value": round(v, 3), "unit": "Mpixel/s", "cores": info["threads"],
-                    "kind": "reference",
-                    "sample": f"one full c{wl.config} frame ({W}x{H}), reference FSE-lite via bit-exact band split",
-                }
-                line["parity"]["exact_bytes_equal_reference"] = bool(np.array_equal(ref_out, ex_out))
-                dr = np.abs(ref_out.astype(int) - fa_out.astype(int))[unk]
-                line["parity"]["fast_within1_of_reference"] = round(float((dr <= 1).mean()), 6)
-            else:
-                line["cpu_baseline"] = None
-        except Exception as e:  # pragma: no cover
-            line["cpu_baseline"] = {"error": str(e)[:200]}
     if rank == 0:
+        ex_out = res["out"] if args.mode == "exact" else res_other["out"]
+        fa_out = res["out"] if args.mode == "fast" else res_other["out"]
+        unk = kn_np == 0
+        dd = np.abs(ex_out.astype(int) - fa_out.astype(int))[unk]
+        qe = ctx.quality(img_np, ex_out, kn_np)
+        qf = ctx.quality(img_np, fa_out, kn_np)
+        pe = [q["psnr"] for q in qe]
+        pf = [q["psnr"] for q in qf]
+        parity = {"fast_within1_of_exact": round(float((dd <= 1).mean()), 6) if dd.size else 1.0,
+                  "fast_max_abs_diff": int(dd.max()) if dd.size else 0,
+                  "psnr_exact_db": [round(x, 4) for x in pe], "psnr_fast_db": [round(x, 4) for x in pf],
+                  "fast_dpsnr_db": round(max(abs(a - b) for a, b in zip(pe, pf)), 5),
+                  "ssim_exact": [round(q["ssim"], 6) for q in qe], "ssim_fast": [round(q["ssim"], 6) for q in qf],
+                  "metrics_source": "GPU tf_quality (metrics.hpp restated)",
+                  "tolerance": ">= 0.999 within +-1 and |dPSNR| <= 0.05 dB per image (north star)"}
+        parity["fast_within_tolerance"] = bool(parity["fast_within1_of_exact"] >= 0.999
+                                               and parity["fast_dpsnr_db"] <= 0.05)
+        line["parity"] = parity
+
+        # ---- CPU baseline: rank 0, N = 1 only, the reference on the host cores
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(wl, img_np, kn_np, ex_out, fa_out, parity)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_baseline(wl, img_np, kn_np, ex_out, fa_out, parity):
+    """The compiled reference (oracle/_ref) on this box's host cores:
+    (1) all host threads via the bit-exact band split on a bounded sample; (2) the as-shipped
+    tile-parallel run_local(workers = tiles) on the c1-c3 frames."""
+    try:
+        import oracle as O
+        if not O.have_ref():
+            return None
+        threads = os.cpu_count() or 1
+        host = host_info()
+        # bounded samples (~10-30 s of CPU work): whole frame for c1-c3, 2 of 8 tiles for c4,
+        # 2 of 64 frames for c5
+        if wl.config in (1, 2, 3):
+            part, n_parts, frames = 0, 1, wl.frames
+        elif wl.config == 4:
+            part, n_parts, frames = 0, 4, 1
+        else:
+            part, n_parts, frames = 0, 1, 2
+        img, kn = img_np[:frames], kn_np[:frames]
+        out = img.copy()
+        t0 = time.perf_counter()
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, out=out, part=part, n_parts=n_parts)
+        dt = time.perf_counter() - t0
+        from dataclasses import replace
+        pix = ref_core_pixels(replace(wl, frames=frames), part, n_parts)
+        v = pix / dt / 1e6
+        res = {"value": round(v, 4), "unit": "Mpixel/s", "cores": threads, "kind": "reference",
+               "sample": (f"{frames} frame(s), tiles t % {n_parts} == {part} of the c{wl.config} workload "
+                          f"({pix} core pixels, {dt:.1f} s), reference fse_lite_extrapolate via the bit-exact "
+                          f"B-aligned band split over all host threads"), **host}
+        if n_parts == 1:
+            parity["exact_bytes_equal_reference"] = bool(np.array_equal(out, ex_out[:frames]))
+            dr = np.abs(out.astype(int) - fa_out[:frames].astype(int))[kn == 0]
+            parity["fast_within1_of_reference"] = round(float((dr <= 1).mean()), 6) if dr.size else 1.0
+        if wl.config in (1, 2, 3):  # as shipped: run_local, one worker thread per tile
+            t0 = time.perf_counter()
+            o2, total_us = O.ref_run_local(img[0], kn[0], *ref_args(wl), workers=wl.tiles)
+            dt2 = time.perf_counter() - t0
+            res["as_shipped"] = {"value": round(wl.W * wl.H / dt2 / 1e6, 4), "unit": "Mpixel/s",
+                                 "cores": wl.tiles, "call": f"run_local(tiles={wl.tiles}, d={wl.overlap}, "
+                                 f"workers={wl.tiles}) on frame 0", "run_stats_total_us": total_us,
+                                 "bytes_equal_all_cores_split": bool(np.array_equal(o2, out[0]))}
+        return res
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)[:200]}
 
 
 if __name__ == "__main__":

@@ -136,9 +136,11 @@ int tf_fse_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
                        const tf_fse_params* p, uint8_t* out);
 
 /* run_master equivalent: plan -> expand -> FSE per halo -> crop -> merge, for
- * `frames` stacked W x H frames.  Tiles (frame-major) are spread over the
- * context's GPUs round-robin (runtime.hpp:102); cores are gathered to the
- * first GPU over NCCL, then copied to `out`.  Output is independent of the
+ * `frames` stacked W x H frames.  The (frame, tile) units are assigned to the
+ * context's GPUs by LPT on core pixels (replaces the reference's i mod n,
+ * runtime.hpp:102; equal costs give that round robin); every GPU receives only
+ * the halo rectangles of its units (overlap.hpp:37-49), cores are gathered to
+ * the first GPU over NCCL, then copied to `out`.  Output is independent of the
  * GPU count.  stats may be NULL. */
 int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
                          int frames, int tiles, int overlap, const tf_fse_params* p,
@@ -147,10 +149,14 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
 /* Device-resident variant on GPU `gpu` of the context: d_img/d_known/d_out
  * are device pointers on that GPU (d_out may alias nothing else); work is
  * enqueued on `stream` (a cudaStream_t, NULL = the context's stream) and NOT
- * synchronised (graph-capturable).  Only tiles t with t % n_parts == part
- * are computed (part/n_parts implement a multi-rank split; 0/1 = all);
- * known pixels of the whole image are copied to d_out.  stats may be NULL
- * (filling it synchronises the stream). */
+ * synchronised.  A call made while `stream` is capturing a CUDA graph is
+ * refused (TF_EINVAL); instead, the second of identical repeated calls is
+ * captured by the library and later identical calls replay that graph.  Calls
+ * on different streams are ordered by the library (each waits for the
+ * previous call's kernels, which share per-GPU scratch).  Only the units that
+ * tf_core_layout assigns to `part` of n_parts are computed (LPT on core pixels;
+ * 0/1 = all); known pixels of the whole image are copied to d_out.  stats may
+ * be NULL (filling it synchronises the stream). */
 int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img,
                                 const uint8_t* d_known, int W, int H, int frames, int tiles,
                                 int overlap, const tf_fse_params* p, int part, int n_parts,
@@ -207,6 +213,12 @@ int tf_fse_kernel_times(tf_ctx* ctx, int gpu, float* out_ms, int max_n);
 /* FP64 DFMA peak (TFLOP/s) and shared-memory LDS.128 bandwidth (TB/s) of a
  * device, measured with calibration kernels (roofline denominators). */
 int tf_calibrate(int device, double* fp64_tflops, double* smem_tbs);
+/* As tf_calibrate plus the FP64 tensor-core rate (mma.sync m8n8k4 .f64), the
+ * FP64 datapath's measured maximum; any output may be NULL. */
+int tf_calibrate_peaks(int device, double* dfma_tflops, double* dmma_tflops, double* smem_tbs);
+/* Kernels this context has enqueued on GPU `gpu` so far (CUDA-graph replays
+ * count their captured kernels). */
+int tf_kernel_launches(tf_ctx* ctx, int gpu, int64_t* total);
 /* Self-test: the FSE kernel's hoisted-reciprocal division must be bit-identical
  * to IEEE a/b; counts mismatches over n hashed operand pairs (expect 0). */
 int tf_selftest_div(int device, int64_t n, uint64_t seed, int64_t* mismatches);
@@ -221,16 +233,28 @@ int tf_comm_init(tf_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
 int tf_comm_gather(tf_ctx* ctx, const void* d_send, void* d_recv, int64_t bytes, int root,
                    void* stream);
 /* Host-side layout of the core gather (no GPU needed): for the frames*tiles
- * units (frame-major) gives each core rect, its frame, its owner part
- * (t % n_parts, runtime.hpp:102) and its byte offset inside the owner's packed
- * payload; part_bytes[n_parts] receives each payload size. Any output may be NULL. */
+ * units (frame-major) gives each core rect, its frame, its owner part (LPT on
+ * core pixels, ties by unit index, to the least-loaded part; replaces i mod n
+ * of runtime.hpp:102) and its byte offset inside the owner's packed payload;
+ * part_bytes[n_parts] receives each payload size. Any output may be NULL. */
 int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* cores,
                    int32_t* frame_of, int32_t* owner, int64_t* offs, int64_t* part_bytes);
-/* Gather the cores of tiles owned by each rank (t % nranks == rank) from every
- * rank's d_img-sized buffer into root's d_out (same layout).  Packs, gathers
- * and unpacks on device. */
+/* Gather the cores of the units each rank owns (tf_core_layout with
+ * n_parts = nranks) from every rank's frame-sized d_out into root's d_out
+ * (same layout; run_master's collect + merge_into, runtime.hpp:112-130).
+ * Packs, NCCL send/recv and unpacks on device, enqueued on `stream`. */
 int tf_comm_gather_cores(tf_ctx* ctx, uint8_t* d_out, int W, int H, int frames, int tiles,
                          int root, void* stream);
+/* One rank of a one-process-per-GPU job on HOST buffers (the run_master /
+ * worker pair of runtime.hpp:60-139 for this rank): H2D of the halo
+ * rectangles of the units this rank owns, FSE on them, NCCL gather of the
+ * cores to `root`, D2H of the merged frames into `out` on root (other ranks
+ * may pass out = NULL).  Without tf_comm_init it runs the whole job on the
+ * context's GPU.  Synchronous.  io_bytes (may be NULL) receives {H2D bytes,
+ * D2H bytes} of this rank. */
+int tf_tiled_extrapolate_rank(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                              int frames, int tiles, int overlap, const tf_fse_params* p, int root,
+                              uint8_t* out, int64_t* io_bytes);
 
 /* ---- synthetic inputs (versioned generator) ---------------- */
 #define TF_SYNTH_VERSION 1

@@ -96,6 +96,8 @@ def ref() -> C.CDLL:
         L.ref_tiled_allcores.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                          C.c_int, C.c_int, C.c_void_p]
+        L.ref_tiled_allcores_part.argtypes = L.ref_tiled_allcores.argtypes[:-1] + [C.c_int, C.c_int, C.c_void_p]
+        L.ref_synth_frame.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.ref_run_local_diffusion.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                               C.c_int, C.c_int, C.c_void_p]
@@ -271,8 +273,18 @@ def ref_run_local(img, known, tiles, overlap, block, margin, iters, gamma, rho, 
     return out, us.value
 
 
+def ref_synth_frame(config, frame, W, H):
+    """The versioned input generator (paper_2207_00238_b200/csrc/synth_gen.hpp) compiled into
+    the reference shim: the same bytes as the product's tf_synth_frame, without loading it."""
+    img = np.empty((H, W), np.uint8)
+    kn = np.empty((H, W), np.uint8)
+    if ref().ref_synth_frame(int(config), int(frame), int(W), int(H), img.ctypes.data, kn.ctypes.data):
+        raise OracleError(1, "ref_synth_frame: bad arguments")
+    return img, kn
+
+
 def ref_tiled_allcores(img, known, tiles, overlap, block, margin, iters, gamma, rho,
-                       threads=None, band_blocks=1, out=None):
+                       threads=None, band_blocks=1, out=None, part=0, n_parts=1):
     img = _u8(img)
     kn = _u8(known)
     if img.ndim == 2:
@@ -282,9 +294,9 @@ def ref_tiled_allcores(img, known, tiles, overlap, block, margin, iters, gamma, 
     if out is None:
         out = img.copy()
     threads = threads or os.cpu_count() or 1
-    rc = ref().ref_tiled_allcores(img.ctypes.data, kn.ctypes.data, W, H, frames, tiles, overlap,
-                                  block, margin, iters, gamma, rho, threads, band_blocks,
-                                  out.ctypes.data)
+    rc = ref().ref_tiled_allcores_part(img.ctypes.data, kn.ctypes.data, W, H, frames, tiles, overlap,
+                                       block, margin, iters, gamma, rho, threads, band_blocks,
+                                       part, n_parts, out.ctypes.data)
     if rc:
         raise OracleError(rc, ref_error())
     return out

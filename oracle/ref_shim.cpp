@@ -15,6 +15,9 @@
 //   ref_tiled_allcores  -> bit-exact band split of fse_lite_extrapolate on a
 //                          thread pool (SURVEY §8(d) "all host cores")
 //   ref_gen_scatter_mask, ref_make_scene, ref_psnr, ref_ssim -> pgm/bench/metrics
+//   ref_synth_frame     -> the repo's versioned input generator (synth_gen.hpp, header-only,
+//                          the same source as the product's tf_synth_frame), so bench.py's
+//                          reference arm builds its inputs without the product library
 
 #include <atomic>
 #include <cstdint>
@@ -25,6 +28,7 @@
 #include <vector>
 
 #include "tframe/tframe.hpp"
+#include "synth_gen.hpp"
 
 namespace {
 
@@ -200,9 +204,11 @@ int ref_run_local(const uint8_t* img, const uint8_t* known, int W, int H, int ti
 // apron is B-aligned and >= margin, every block sees the same grid position and
 // the same clamped support window as in the whole-halo call, so the output is
 // byte-identical to run_local (checked in tests/test_oracle.py).
-int ref_tiled_allcores(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
-                       int tiles, int overlap, int block, int margin, int iters, double gamma,
-                       double rho, int threads, int band_blocks, uint8_t* out) {
+// part/n_parts: only tiles t with t % n_parts == part (a bounded sample for the bench arm).
+int ref_tiled_allcores_part(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
+                            int tiles, int overlap, int block, int margin, int iters, double gamma,
+                            double rho, int threads, int band_blocks, int part, int n_parts,
+                            uint8_t* out) {
   try {
     tframe::FseLiteParams p{block, margin, iters, gamma, rho};
     const tframe::TileLayout layout = tframe::plan_proposed(W, H, tiles);
@@ -214,8 +220,9 @@ int ref_tiled_allcores(const uint8_t* img, const uint8_t* known, int W, int H, i
     std::vector<Task> tasks;
     const int band = block * (band_blocks > 0 ? band_blocks : 1);
     for (int f = 0; f < frames; ++f)
-      for (const auto& t : layout.tiles) {
-        const auto et = tframe::expand(t, overlap, W, H);
+      for (size_t ti = 0; ti < layout.tiles.size(); ++ti) {
+        if (n_parts > 1 && static_cast<int>(ti % static_cast<size_t>(n_parts)) != part) continue;
+        const auto et = tframe::expand(layout.tiles[ti], overlap, W, H);
         for (int y0 = 0; y0 < et.halo.h; y0 += band)
           tasks.push_back(Task{f, et, y0, std::min(et.halo.h, y0 + band)});
       }
@@ -272,6 +279,19 @@ int ref_tiled_allcores(const uint8_t* img, const uint8_t* known, int W, int H, i
   } catch (const std::exception& e) {
     return fail(e, 9);
   }
+}
+
+int ref_tiled_allcores(const uint8_t* img, const uint8_t* known, int W, int H, int frames,
+                       int tiles, int overlap, int block, int margin, int iters, double gamma,
+                       double rho, int threads, int band_blocks, uint8_t* out) {
+  return ref_tiled_allcores_part(img, known, W, H, frames, tiles, overlap, block, margin, iters,
+                                 gamma, rho, threads, band_blocks, 0, 1, out);
+}
+
+int ref_synth_frame(int config, int frame, int W, int H, uint8_t* img, uint8_t* known) {
+  if (config < 1 || config > 5 || frame < 0 || W < 1 || H < 1 || !img || !known) return 1;
+  tfsynth::synth_frame(config, frame, W, H, img, known);
+  return 0;
 }
 
 // diffusion_extrapolate (extrapolate.hpp:41-84) and run_local with algo "diffusion"

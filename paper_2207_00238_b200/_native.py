@@ -73,6 +73,10 @@ SIGNATURES = {
     "tf_tiled_diffusion": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, C.POINTER(tf_run_stats)]),
     "tf_fse_kernel_times": (_i, [_vp, _i, C.POINTER(C.c_float), _i]),
     "tf_calibrate": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tf_calibrate_peaks": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "tf_kernel_launches": (_i, [_vp, _i, C.POINTER(C.c_int64)]),
+    "tf_tiled_extrapolate_rank": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, C.POINTER(tf_fse_params), _i,
+                                       _vp, _vp]),
     "tf_selftest_div": (_i, [_i, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     "tf_comm_unique_id": (_i, [_vp]),
     "tf_comm_init": (_i, [_vp, _i, _i, _vp]),

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libtframe_b200.so"
 SOURCES = ["fse_kernels.cu", "diffusion.cu", "metrics.cu", "capi.cpp", "tiling.cpp", "synth.cpp", "calibrate.cu"]
-HEADERS = ["fse_kernels.cuh", "host_internal.hpp"]
+HEADERS = ["fse_kernels.cuh", "host_internal.hpp", "synth_gen.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -24,6 +24,25 @@ __global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// FP64 tensor-core path (mma.sync m8n8k4 .f64; tcgen05 has no f64 kind): the FP64 datapath's
+// measured maximum (DFMA and DMMA share it, profiles/r1_dmma_bench.txt)
+__global__ void dmma_peak_kernel(double* out, int iters) {
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[kChains][2];
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < kChains; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void lds_peak_kernel(double* out, int iters) {
   __shared__ double2 buf[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_double2(i, -i);
@@ -45,6 +64,38 @@ __global__ void lds_peak_kernel(double* out, int iters) {
 }
 
 }  // namespace
+
+// DMMA m8n8k4: 8 x 8 x 4 MACs = 512 flops per warp instruction
+extern "C" int tf_calibrate_peaks(int device, double* dfma_tflops, double* dmma_tflops, double* smem_tbs) {
+  int rc = tf_calibrate(device, dfma_tflops, smem_tbs);
+  if (rc != TF_OK) return rc;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, 64) != cudaSuccess) return tfh::set_error(TF_ENOMEM, "calibrate alloc");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  const int threads = 128, blocks = sms * 4, iters = 20000;
+  for (int rep = 0; rep < 4; ++rep) {
+    float ms = 0.f;
+    cudaEventRecord(e0);
+    dmma_peak_kernel<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = 512.0 * kChains * iters * (threads / 32) * static_cast<double>(blocks);
+    if (rep && fl / (ms * 1e-3) > best) best = fl / (ms * 1e-3);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return tfh::set_error(TF_ECUDA, cudaGetErrorString(e));
+  if (dmma_tflops) *dmma_tflops = best / 1e12;
+  return TF_OK;
+}
 
 extern "C" int tf_calibrate(int device, double* fp64_tflops, double* smem_tbs) {
   cudaError_t e = cudaSetDevice(device);

@@ -154,6 +154,15 @@ struct Gpu {
   int big_occ = 0;
   DevBuf dfield0, dfield1, dfoff, dpoff;        // diffusion: FP64 fields, tile offsets
   ncclComm_t comm = nullptr;                    // single-process multi-GPU comm
+  // one-process-per-GPU core gather: its own tile table / core offsets (per layout)
+  DevBuf gtiles, goffs;
+  std::string glayout;
+  std::vector<int64_t> gsize;
+  int gtiles_n = 0;
+  int64_t gmax_core = 0;
+  // kernels enqueued by this context on this GPU (graph replays add their captured count)
+  int64_t kl = 0, gexec_kl = 0, hexec_kl = 0;
+  cudaEvent_t ev_work = nullptr;  // end of the last enqueued call: the next call's streams wait on it
   // ring of (start, stop) events around the most recent FSE kernel launches
   static constexpr int kRing = 256;
   cudaEvent_t ring0[kRing] = {}, ring1[kRing] = {};
@@ -240,8 +249,34 @@ struct Plan {
   int64_t max_core = 0;
 };
 
+// Owner of every (frame, tile) unit for an n_parts split: LPT (longest processing time
+// first) with cost = core pixels (the work of a stationary mask), ties by unit index, each
+// unit to the least-loaded part (ties: lowest part).  It depends on (W, H, frames, tiles,
+// n_parts) only -- host-only and mask-, overlap- and block-independent -- so every rank of a
+// one-process-per-GPU job and the core gather derive the same ownership without
+// communication; the output never depends on it (each core is reconstructed from its own
+// halo, runtime.hpp:102-130).  Equal costs give the reference's round robin (i mod n,
+// runtime.hpp:102).
+static void assign_owners(Plan& pl, int n_parts) {
+  const size_t n = pl.tiles.size();
+  std::vector<int> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = static_cast<int>(i);
+  const auto cost = [&](int i) {
+    return static_cast<int64_t>(pl.tiles[static_cast<size_t>(i)].cw) * pl.tiles[static_cast<size_t>(i)].ch;
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  std::vector<int64_t> load(static_cast<size_t>(std::max(n_parts, 1)), 0);
+  for (int u : order) {
+    size_t best = 0;
+    for (size_t q = 1; q < load.size(); ++q)
+      if (load[q] < load[best]) best = q;
+    pl.tiles[static_cast<size_t>(u)].owner = static_cast<int32_t>(best);
+    load[best] += cost(u);
+  }
+}
+
 static int make_plan(int W, int H, int frames, int n_tiles, int overlap, int B, int margin,
-                     Plan& pl) {
+                     Plan& pl, int n_parts = 1) {
   if (W < 1 || H < 1 || frames < 1) return set_error(TF_EINVAL, "image dimensions must be >= 1");
   int rc = plan_proposed(W, H, n_tiles, pl.cores);
   if (rc != TF_OK) return rc;
@@ -287,6 +322,7 @@ static int make_plan(int W, int H, int frames, int n_tiles, int overlap, int B, 
   const int mw = std::min(span, max_hw), mh = std::min(span, max_hh);
   pl.wmax = std::max(mw, mh);
   pl.nmax = mw * mh;
+  assign_owners(pl, n_parts);
   return TF_OK;
 }
 
@@ -534,6 +570,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   e.xblocks = xblocks;
   e.n_xblocks = counters + 4;
   TF_CUDA(tfb::enumerate_launch(e, pl.max_grid, s));
+  ++g.kl;
 
   tfb::FseLaunch a{};
   a.img = d_img;
@@ -563,6 +600,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     const int xg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.occ[1][cfgx],
                                                       std::max<int64_t>(cand, 1)));
     TF_CUDA(tfb::fse_launch(cfgx, true, x, xg, xsmem, st));
+    ++g.kl;
     return TF_OK;
   };
   int grid = g.sms * g.occ[exact][cfg];
@@ -593,6 +631,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     const bool border_after = std::getenv("TF_GEN_BEFORE") ? false : !graph;  // as in the warp-kernel branch
     if (!border_after) {
       TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+      ++g.kl;
       TF_CUDA(cudaEventRecord(g.ev_join, side));
     }
     const int wgrid = g.sms * g.wide_occ[w64][wide];
@@ -609,8 +648,10 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(tfb::fse_wide_launch(wide, w64, w,
                                  static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1))),
                                  wide_smem, s));
+    ++g.kl;
     if (border_after) {
       TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+      ++g.kl;
       TF_CUDA(cudaEventRecord(g.ev_join, side));
     }
     TF_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
@@ -619,8 +660,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
     const int wgrid = g.sms * g.wocc[exact][wbpt];
-    const int ggrid = gbpth ? std::min(g.sms * g.gocc[gbpth], std::max(grid, 1)) : 0;
-    const size_t per = static_cast<size_t>(wgrid + ggrid) * p.iters;  // log entries per band slot
+    // log entries per band slot: sized from band-independent bounds (bands run concurrently
+    // on their own streams, slot k at k * per)
+    const int ggrid_cap = gbpth ? static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.gocc[gbpth],
+                                                                     std::max<int64_t>(pl.cand_blocks, 1)))
+                                : 0;
+    const int ggrid = gbpth ? std::min(ggrid_cap, std::max(grid, 1)) : 0;
+    const size_t per = static_cast<size_t>(wgrid + ggrid_cap) * p.iters;
     TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
     TF_CUDA(g.wlog_c.ensure(nslots * per * sizeof(double2)));
     const auto launch_border = [&]() -> int {
@@ -629,8 +675,10 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
         ga.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
         ga.wlog_c = g.wlog_c.as<double2>() + bslot * per + static_cast<size_t>(wgrid) * p.iters;
         TF_CUDA(tfb::fse_half_launch(0, gbpth, ga, ggrid, gsmem, side));
+        ++g.kl;
       } else {
         TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
+        ++g.kl;
       }
       TF_CUDA(cudaEventRecord(g.ev_join, side));
       return TF_OK;
@@ -656,10 +704,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       const int pg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.pair_occ,
                                                         std::max<int64_t>((cand + 1) / 2, 1)));
       TF_CUDA(tfb::fse_pair_launch(pair, w, pg, pair_smem, s));
+      ++g.kl;
     } else if (wkind == 1) {
       TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wg, wsmem, s));
+      ++g.kl;
     } else {
       TF_CUDA(tfb::fse_half_launch(hnt, wbpt, w, wg, wsmem, s));
+      ++g.kl;
     }
     if (border_after) {
       rc = launch_border();
@@ -669,16 +720,20 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   } else if (big) {
     // per-CTA scratch, at most ~4 GB per band slot
     const tfb::BigLayout bl(pl.nmax, p.iters);
-    int64_t bg = std::min<int64_t>(static_cast<int64_t>(g.sms) * g.big_occ, std::max<int64_t>(cand, 1));
-    bg = std::max<int64_t>(1, std::min<int64_t>(bg, (int64_t{4} << 30) / static_cast<int64_t>(bl.total)));
-    const size_t per = static_cast<size_t>(bg) * bl.total;
+    // scratch per band slot from a band-independent bound (concurrent bands, slot k at k * per)
+    int64_t bg_cap = std::min<int64_t>(static_cast<int64_t>(g.sms) * g.big_occ, std::max<int64_t>(pl.cand_blocks, 1));
+    bg_cap = std::max<int64_t>(1, std::min<int64_t>(bg_cap, (int64_t{4} << 30) / static_cast<int64_t>(bl.total)));
+    const int64_t bg = std::max<int64_t>(1, std::min<int64_t>(bg_cap, cand));
+    const size_t per = static_cast<size_t>(bg_cap) * bl.total;
     TF_CUDA(g.big.ensure(nslots * per));
     tfb::FseLaunch b = a;
     b.scratch = g.big.as<unsigned char>() + bslot * per;
     b.nmax = pl.nmax;
     TF_CUDA(tfb::fse_big_launch(b, static_cast<int>(bg), s));
+    ++g.kl;
   } else {
     TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, s));
+    ++g.kl;
   }
 
   if (!x_first) {
@@ -710,7 +765,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
                        cudaMemcpyDeviceToHost));
     res->ref_blocks = 0;
     for (size_t t = 0; t < n_tiles; ++t)
-      if (static_cast<int>(t % n_parts) == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
+      if (pl.tiles[t].owner == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
     res->processed = cnt[0] + cnt[2] + cnt[4];
     std::vector<BlockStat> st(static_cast<size_t>(cnt[0] + cnt[2] + cnt[4]));
     if (cnt[0] > 0)
@@ -827,16 +882,79 @@ static int64_t us_since(clk::time_point a) {
 }
 
 // Core offsets: tile t's core goes to offs[t] inside the payload of its owner
-// (t % n_parts); returns per-owner payload sizes.
+// (pl.tiles[t].owner); returns per-owner payload sizes.
 static std::vector<int64_t> core_offsets(const Plan& pl, int n_parts, std::vector<int64_t>& offs) {
   std::vector<int64_t> size(static_cast<size_t>(n_parts), 0);
   offs.resize(pl.tiles.size());
   for (size_t t = 0; t < pl.tiles.size(); ++t) {
-    const int o = static_cast<int>(t % n_parts);
+    const int o = pl.tiles[t].owner;
     offs[t] = size[o];
     size[o] += static_cast<int64_t>(pl.tiles[t].cw) * pl.tiles[t].ch;
   }
   return size;
+}
+
+// NCCL gather of the core rectangles of a one-process-per-GPU job to `root` (run_master's
+// collect + merge_into, runtime.hpp:112-130): every rank packs the cores it owns
+// (cores_kernel) and sends them; the root receives each rank's payload and unpacks it into
+// d_out.  The tile table and core offsets live in the gather's own device buffers, staged
+// once per layout, so the gather never touches the FSE path's tile table or pinned staging
+// (which that path's CUDA graph reads on every replay).
+static int gather_cores(tf_ctx* ctx, Gpu& g, uint8_t* d_out, int W, int H, int frames, int tiles,
+                        int root, cudaStream_t s) {
+  Nccl& nc = nccl();
+  if (!nc.ok) return set_error(TF_ENCCL, nc.why);
+  const int n = ctx->nranks;
+  char kb[128];
+  std::snprintf(kb, sizeof(kb), "%d %d %d %d %d", W, H, frames, tiles, n);
+  if (g.glayout != kb) {
+    Plan pl;
+    const int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl, n);
+    if (rc != TF_OK) return rc;
+    std::vector<int64_t> offs;
+    g.gsize = core_offsets(pl, n, offs);
+    g.gtiles_n = static_cast<int>(pl.tiles.size());
+    g.gmax_core = pl.max_core;
+    TF_CUDA(cudaDeviceSynchronize());  // earlier gathers may still read the old tables
+    TF_CUDA(g.gtiles.ensure(pl.tiles.size() * sizeof(TileDesc)));
+    TF_CUDA(g.goffs.ensure(offs.size() * sizeof(int64_t)));
+    TF_CUDA(cudaMemcpy(g.gtiles.p, pl.tiles.data(), pl.tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+    TF_CUDA(cudaMemcpy(g.goffs.p, offs.data(), offs.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    g.glayout = kb;
+  }
+  const std::vector<int64_t>& size = g.gsize;
+  if (ctx->rank == root) {
+    int64_t total = 0;
+    std::vector<int64_t> base(static_cast<size_t>(n), 0);
+    for (int q = 0; q < n; ++q)
+      if (q != root) {
+        base[static_cast<size_t>(q)] = total;
+        total += size[static_cast<size_t>(q)];
+      }
+    TF_CUDA(g.recv.ensure(static_cast<size_t>(std::max<int64_t>(total, 1))));
+    TF_NCCL(nc.GroupStart());
+    for (int q = 0; q < n; ++q)
+      if (q != root && size[static_cast<size_t>(q)])
+        TF_NCCL(nc.Recv(g.recv.as<uint8_t>() + base[static_cast<size_t>(q)],
+                        static_cast<size_t>(size[static_cast<size_t>(q)]), ncclUint8, q, ctx->rank_comm, s));
+    TF_NCCL(nc.GroupEnd());
+    for (int q = 0; q < n; ++q)
+      if (q != root && size[static_cast<size_t>(q)]) {
+        TF_CUDA(tfb::cores_launch(d_out, W, H, g.gtiles.as<TileDesc>(), g.gtiles_n, q, n, g.goffs.as<int64_t>(),
+                                  g.recv.as<uint8_t>() + base[static_cast<size_t>(q)], true, g.gmax_core, s));
+        ++g.kl;
+      }
+  } else {
+    const size_t sz = static_cast<size_t>(size[static_cast<size_t>(ctx->rank)]);
+    TF_CUDA(g.packed.ensure(std::max<size_t>(sz, 1)));
+    if (sz) {
+      TF_CUDA(tfb::cores_launch(d_out, W, H, g.gtiles.as<TileDesc>(), g.gtiles_n, ctx->rank, n,
+                                g.goffs.as<int64_t>(), g.packed.as<uint8_t>(), false, g.gmax_core, s));
+      ++g.kl;
+      TF_NCCL(nc.Send(g.packed.p, sz, ncclUint8, root, ctx->rank_comm, s));
+    }
+  }
+  return TF_OK;
 }
 
 }  // namespace tfh
@@ -888,7 +1006,8 @@ tf_ctx* tf_create(int n_gpus, const int* device_ids) {
         cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&g.ev0) != cudaSuccess || cudaEventCreate(&g.ev1) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g.ev_tables, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&g.ev_tables, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g.ev_work, cudaEventDisableTiming) != cudaSuccess) {
       set_error(TF_ECUDA, "tf_create: stream/event creation failed");
       return nullptr;
     }
@@ -906,7 +1025,8 @@ void tf_destroy(tf_ctx* ctx) {
     if (g.hexec) cudaGraphExecDestroy(g.hexec);
     if (g.ev_gstart) cudaEventDestroy(g.ev_gstart);
     if (g.ev_cout) cudaEventDestroy(g.ev_cout);
-    for (DevBuf* b : {&g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
+    if (g.ev_work) cudaEventDestroy(g.ev_work);
+    for (DevBuf* b : {&g.gtiles, &g.goffs, &g.img, &g.known, &g.out, &g.tiles, &g.blocks, &g.counters, &g.refblk,
                       &g.stats, &g.rho, &g.tw, &g.offs, &g.packed, &g.recv, &g.wblocks,
                       &g.wlog_kl, &g.wlog_c, &g.qbuf, &g.xblocks, &g.big, &g.dfield0, &g.dfield1,
                       &g.dfoff, &g.dpoff})
@@ -970,7 +1090,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
   if (rc != TF_OK) return rc;
   const auto t0 = clk::now();
   Plan pl;
-  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl, n_parts);
   if (rc != TF_OK) return rc;
   const int64_t plan_us = us_since(t0);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
@@ -998,10 +1118,13 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
       if (rc != TF_OK) return rc;
       g.last_key = key;
       cudaGraph_t graph = nullptr;
+      const int64_t kl0 = g.kl;
       TF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
       rc = run_device(ctx, g, pl, d_img, d_known, W, H, frames, *p, part, n_parts, d_out, s, false,
                       nullptr, nullptr, true);
       const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      g.gexec_kl = g.kl - kl0;  // captured, not run: counted at every replay
+      g.kl = kl0;
       if (rc != TF_OK) {
         if (graph) cudaGraphDestroy(graph);
         return rc;
@@ -1021,12 +1144,15 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
         TF_CUDA(cudaEventCreate(&g.ring0[slot]));
         TF_CUDA(cudaEventCreate(&g.ring1[slot]));
       }
+      TF_CUDA(cudaStreamWaitEvent(s, g.ev_work, 0));  // the previous call's kernels (any stream)
       TF_CUDA(cudaEventRecord(g.ev0, s));
       TF_CUDA(cudaEventRecord(g.ring0[slot], s));
       TF_CUDA(cudaGraphLaunch(g.gexec, s));
+      g.kl += g.gexec_kl;
       TF_CUDA(cudaEventRecord(g.ev_tables, s));  // the pinned tile table is read by the graph
       TF_CUDA(cudaEventRecord(g.ring1[slot], s));
       TF_CUDA(cudaEventRecord(g.ev1, s));
+      TF_CUDA(cudaEventRecord(g.ev_work, s));
       ++g.launches;
       return TF_OK;
     }
@@ -1038,9 +1164,13 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
     if (rc != TF_OK) return rc;
   }
   DevRun dr;
+  // per-GPU scratch (tile table, counters, block lists, logs) is reused by every call: wait
+  // for the previous call's kernels, whichever stream they were enqueued on
+  TF_CUDA(cudaStreamWaitEvent(s, g.ev_work, 0));
   rc = run_device(ctx, g, pl, d_img, d_known, W, H, frames, *p, part, n_parts, d_out, s,
                   stats != nullptr, &dr);
   if (rc != TF_OK) return rc;
+  TF_CUDA(cudaEventRecord(g.ev_work, s));
   if (stats) {
     *stats = tf_run_stats{};
     stats->plan_us = plan_us;
@@ -1123,8 +1253,10 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
       TF_CUDA(cudaStreamWaitEvent(g.bside[k], g.ev_gstart, 0));
     }
   } else {
-    // the previous call's copy-out must be done with g.out before it is overwritten
+    // the previous call's copy-out must be done with g.out before it is overwritten, and the
+    // previous call's kernels (any stream) with the per-GPU scratch
     TF_CUDA(cudaStreamSynchronize(g.cout));
+    TF_CUDA(cudaStreamWaitEvent(g.cin, g.ev_work, 0));
   }
   // copy-in in finer chunks than the compute bands: a band waits only for the chunk that
   // holds the last row its windows reach
@@ -1219,6 +1351,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     return TF_OK;
   }
   TF_CUDA(cudaEventRecord(g.ev1, g.stream));
+  TF_CUDA(cudaEventRecord(g.ev_work, g.stream));
   const auto t_enq = clk::now();
   TF_CUDA(cudaStreamSynchronize(g.cout));
   TF_CUDA(cudaStreamSynchronize(g.stream));
@@ -1241,6 +1374,24 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
     std::fprintf(stderr, "[tframe] streamed %d bands: enqueue %lld us, total %lld us, compute span %.1f us\n",
                  nb, static_cast<long long>(std::chrono::duration_cast<std::chrono::microseconds>(t_enq - t_start).count()),
                  static_cast<long long>(us_since(t_start)), ms * 1e3);
+  }
+  return TF_OK;
+}
+
+// H2D of the halo rectangles (image + mask) of the units `part` owns into frame-shaped device
+// buffers at their frame offsets (the reference's extract, overlap.hpp:37-49, without the
+// re-layout: the kernels index the frame with the halo origin).  Overlapping halos of one
+// owner are copied once per unit (a few aprons).  *bytes_out += host bytes read.
+static int upload_halos(Gpu& g, const Plan& pl, int part, const uint8_t* img, const uint8_t* known,
+                        int W, int H, cudaStream_t s, int64_t* bytes_out) {
+  const size_t plane = static_cast<size_t>(W) * H;
+  for (const TileDesc& t : pl.tiles) {
+    if (t.owner != part) continue;
+    const size_t off = plane * t.frame + static_cast<size_t>(t.hy) * W + t.hx;
+    TF_CUDA(cudaMemcpy2DAsync(g.img.as<uint8_t>() + off, W, img + off, W, t.hw, t.hh, cudaMemcpyHostToDevice, s));
+    TF_CUDA(cudaMemcpy2DAsync(g.known.as<uint8_t>() + off, W, known + off, W, t.hw, t.hh,
+                              cudaMemcpyHostToDevice, s));
+    if (bytes_out) *bytes_out += 2 * static_cast<int64_t>(t.hw) * t.hh;
   }
   return TF_OK;
 }
@@ -1326,10 +1477,10 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
   }
   const auto t0 = clk::now();
   Plan pl;
-  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl);
+  const int n = static_cast<int>(ctx->gpus.size());
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl, n);
   if (rc != TF_OK) return rc;
   const int64_t plan_us = us_since(t0);
-  const int n = static_cast<int>(ctx->gpus.size());
   const size_t bytes = static_cast<size_t>(W) * H * frames;
   // ---- one GPU: streamed row bands (copy-in / compute / copy-out overlap), unless the
   // frames are too short to split (TF_STREAM_BANDS overrides the band count, 1 = one shot)
@@ -1375,9 +1526,12 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       if (rc != TF_OK) return rc;
       TF_CUDA(cudaStreamSynchronize(g.cout));  // previous call's copy-out (outside the capture)
       cudaGraph_t graph = nullptr;
+      const int64_t kl0 = g.kl;
       TF_CUDA(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeRelaxed));
       rc = run_streamed(ctx, g, pl, img, known, W, H, frames, *p, out, nbands, true);
       const cudaError_t ce = cudaStreamEndCapture(g.stream, &graph);
+      g.hexec_kl = g.kl - kl0;
+      g.kl = kl0;
       if (rc != TF_OK) {
         if (graph) cudaGraphDestroy(graph);
         return rc;
@@ -1392,8 +1546,10 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       g.hkey = key;
     }
     if (!key.empty() && g.hexec && g.hkey == key) {
+      TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_work, 0));
       TF_CUDA(cudaEventRecord(g.ev0, g.stream));
       TF_CUDA(cudaGraphLaunch(g.hexec, g.stream));
+      g.kl += g.hexec_kl;
       TF_CUDA(cudaEventRecord(g.ev_tables, g.stream));  // host-waitable again after the capture
       TF_CUDA(cudaEventRecord(g.ev1, g.stream));
       TF_CUDA(cudaStreamSynchronize(g.stream));
@@ -1430,7 +1586,9 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     rc = drop_graph(gd);
     if (rc != TF_OK) return rc;
   }
-  // ---- distribute: H2D on every GPU, enqueue enumeration + FSE
+  // ---- distribute: every GPU receives only the halo rectangles of the tiles it owns
+  // (overlap.hpp:37-49 extract, as 2-D copies into a frame-shaped buffer so the kernels index
+  // it like the whole frame), then enqueue enumeration + FSE
   std::vector<DevRun> dr(static_cast<size_t>(n));
   for (int gi = 0; gi < n; ++gi) {
     Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
@@ -1439,11 +1597,18 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     TF_CUDA(g.img.ensure(bytes));
     TF_CUDA(g.known.ensure(bytes));
     TF_CUDA(g.out.ensure(bytes));
-    TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
-    TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+    TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_work, 0));
+    if (n == 1) {
+      TF_CUDA(cudaMemcpyAsync(g.img.p, img, bytes, cudaMemcpyHostToDevice, g.stream));
+      TF_CUDA(cudaMemcpyAsync(g.known.p, known, bytes, cudaMemcpyHostToDevice, g.stream));
+    } else {
+      rc = upload_halos(g, pl, gi, img, known, W, H, g.stream, nullptr);
+      if (rc != TF_OK) return rc;
+    }
     rc = run_device(ctx, g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, *p, gi,
                     n, g.out.as<uint8_t>(), g.stream, false, nullptr);
     if (rc != TF_OK) return rc;
+    TF_CUDA(cudaEventRecord(g.ev_work, g.stream));
   }
   const auto t_dispatched = clk::now();
   const int64_t distribute_us = us_since(t0) - plan_us;
@@ -1470,7 +1635,7 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));
       for (size_t t = 0; t < ref.size(); ++t)
-        if (static_cast<int>(t % n) == gi) stats->blocks_reference += static_cast<int64_t>(ref[t]);
+        if (pl.tiles[t].owner == gi) stats->blocks_reference += static_cast<int64_t>(ref[t]);
     }
     stats->kernel_ms = kms;
   }
@@ -1487,7 +1652,7 @@ static int run_device_diffusion(Gpu& g, const Plan& pl, const uint8_t* d_img, co
   int64_t fsum = 0, psum = 0, max_core = 0;
   int max_halo = 0;
   for (size_t t = 0; t < pl.tiles.size(); ++t) {
-    if (static_cast<int>(t % static_cast<size_t>(n_parts)) != part) continue;
+    if (pl.tiles[t].owner != part) continue;
     const TileDesc& d = pl.tiles[t];
     mine.push_back(d);
     foff.push_back(fsum);
@@ -1553,10 +1718,10 @@ int tf_tiled_diffusion(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, in
   }
   const auto t0 = clk::now();
   Plan pl;
-  rc = make_plan(W, H, frames, tiles, overlap, 1, 0, pl);  // block grid unused
+  const int n = static_cast<int>(ctx->gpus.size());
+  rc = make_plan(W, H, frames, tiles, overlap, 1, 0, pl, n);  // block grid unused
   if (rc != TF_OK) return rc;
   const int64_t plan_us = us_since(t0);
-  const int n = static_cast<int>(ctx->gpus.size());
   const size_t bytes = static_cast<size_t>(W) * H * frames;
   for (int gi = 0; gi < n; ++gi) {
     Gpu& g = ctx->gpus[static_cast<size_t>(gi)];
@@ -1730,7 +1895,7 @@ int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* co
                    int32_t* frame_of, int32_t* owner, int64_t* offs, int64_t* part_bytes) {
   if (n_parts < 1) return set_error(TF_EINVAL, "n_parts must be >= 1");
   Plan pl;
-  const int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl);
+  const int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl, n_parts);
   if (rc != TF_OK) return rc;
   std::vector<int64_t> o;
   const std::vector<int64_t> size = core_offsets(pl, n_parts, o);
@@ -1738,7 +1903,7 @@ int tf_core_layout(int W, int H, int frames, int tiles, int n_parts, tf_rect* co
     const TileDesc& d = pl.tiles[t];
     if (cores) cores[t] = tf_rect{d.cx, d.cy, d.cw, d.ch};
     if (frame_of) frame_of[t] = d.frame;
-    if (owner) owner[t] = static_cast<int32_t>(t % static_cast<size_t>(n_parts));
+    if (owner) owner[t] = d.owner;
     if (offs) offs[t] = o[t];
   }
   if (part_bytes) std::copy(size.begin(), size.end(), part_bytes);
@@ -1811,60 +1976,67 @@ int tf_comm_gather(tf_ctx* ctx, const void* d_send, void* d_recv, int64_t bytes,
   return TF_OK;
 }
 
+int tf_kernel_launches(tf_ctx* ctx, int gpu, int64_t* total) {
+  if (!ctx || gpu < 0 || gpu >= static_cast<int>(ctx->gpus.size()) || !total)
+    return set_error(TF_EINVAL, "bad arguments");
+  *total = ctx->gpus[static_cast<size_t>(gpu)].kl;
+  return TF_OK;
+}
+
+int tf_tiled_extrapolate_rank(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, int W, int H,
+                              int frames, int tiles, int overlap, const tf_fse_params* p, int root,
+                              uint8_t* out, int64_t* io_bytes) {
+  if (!ctx || ctx->gpus.size() != 1) return set_error(TF_EINVAL, "tf_tiled_extrapolate_rank needs a 1-GPU context");
+  int rc = check_params(p);
+  if (rc != TF_OK) return rc;
+  const int nr = ctx->rank_comm ? ctx->nranks : 1, rk = ctx->rank_comm ? ctx->rank : 0;
+  if (root < 0 || root >= nr) return set_error(TF_EINVAL, "bad root");
+  if (!img || !known || (rk == root && !out)) return set_error(TF_EINVAL, "null buffer");
+  Gpu& g = ctx->gpus[0];
+  rc = select_device(g);
+  if (rc != TF_OK) return rc;
+  Plan pl;
+  rc = make_plan(W, H, frames, tiles, overlap, p->block, p->margin, pl, nr);
+  if (rc != TF_OK) return rc;
+  rc = drop_graph(g);  // the tile table is restaged below
+  if (rc != TF_OK) return rc;
+  const size_t bytes = static_cast<size_t>(W) * H * frames;
+  TF_CUDA(g.img.ensure(bytes));
+  TF_CUDA(g.known.ensure(bytes));
+  TF_CUDA(g.out.ensure(bytes));
+  TF_CUDA(cudaStreamWaitEvent(g.stream, g.ev_work, 0));
+  int64_t h2d = 0, d2h = 0;
+  rc = upload_halos(g, pl, rk, img, known, W, H, g.stream, &h2d);
+  if (rc != TF_OK) return rc;
+  rc = run_device(ctx, g, pl, g.img.as<uint8_t>(), g.known.as<uint8_t>(), W, H, frames, *p, rk, nr,
+                  g.out.as<uint8_t>(), g.stream, false, nullptr);
+  if (rc != TF_OK) return rc;
+  if (nr > 1) {
+    rc = gather_cores(ctx, g, g.out.as<uint8_t>(), W, H, frames, tiles, root, g.stream);
+    if (rc != TF_OK) return rc;
+  }
+  if (rk == root) {
+    TF_CUDA(cudaMemcpyAsync(out, g.out.p, bytes, cudaMemcpyDeviceToHost, g.stream));
+    d2h = static_cast<int64_t>(bytes);
+  }
+  TF_CUDA(cudaEventRecord(g.ev_work, g.stream));
+  TF_CUDA(cudaStreamSynchronize(g.stream));
+  if (io_bytes) {
+    io_bytes[0] = h2d;
+    io_bytes[1] = d2h;
+  }
+  return TF_OK;
+}
+
 int tf_comm_gather_cores(tf_ctx* ctx, uint8_t* d_out, int W, int H, int frames, int tiles,
                          int root, void* stream) {
   if (!ctx || !ctx->rank_comm) return set_error(TF_EINVAL, "no communicator (tf_comm_init)");
-  Plan pl;
-  int rc = make_plan(W, H, frames, tiles, 0, 2, 0, pl);
-  if (rc != TF_OK) return rc;
-  Nccl& nc = nccl();
+  if (!d_out) return set_error(TF_EINVAL, "null buffer");
+  if (root < 0 || root >= ctx->nranks) return set_error(TF_EINVAL, "bad root");
   Gpu& g = ctx->gpus[0];
   TF_CUDA(cudaSetDevice(g.dev));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g.stream;
-  const int n = ctx->nranks;
-  std::vector<int64_t> offs;
-  const std::vector<int64_t> size = core_offsets(pl, n, offs);
-  if (g.ev_tables) TF_CUDA(cudaEventSynchronize(g.ev_tables));
-  const size_t tb = pl.tiles.size() * sizeof(TileDesc), ob = offs.size() * sizeof(int64_t);
-  rc = ensure_pinned(g, tb + ob);
-  if (rc != TF_OK) return rc;
-  std::memcpy(g.pinned, pl.tiles.data(), tb);
-  std::memcpy(static_cast<uint8_t*>(g.pinned) + tb, offs.data(), ob);
-  TF_CUDA(g.tiles.ensure(tb));
-  TF_CUDA(g.offs.ensure(ob));
-  TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, tb, cudaMemcpyHostToDevice, s));
-  TF_CUDA(cudaMemcpyAsync(g.offs.p, static_cast<uint8_t*>(g.pinned) + tb, ob, cudaMemcpyHostToDevice, s));
-  TF_CUDA(cudaEventRecord(g.ev_tables, s));
-  const int nt = static_cast<int>(pl.tiles.size());
-  if (ctx->rank == root) {
-    int64_t total = 0;
-    std::vector<int64_t> base(static_cast<size_t>(n), 0);
-    for (int q = 0; q < n; ++q)
-      if (q != root) {
-        base[static_cast<size_t>(q)] = total;
-        total += size[static_cast<size_t>(q)];
-      }
-    TF_CUDA(g.recv.ensure(static_cast<size_t>(std::max<int64_t>(total, 1))));
-    TF_NCCL(nc.GroupStart());
-    for (int q = 0; q < n; ++q)
-      if (q != root && size[static_cast<size_t>(q)])
-        TF_NCCL(nc.Recv(g.recv.as<uint8_t>() + base[static_cast<size_t>(q)],
-                        static_cast<size_t>(size[static_cast<size_t>(q)]), ncclUint8, q,
-                        ctx->rank_comm, s));
-    TF_NCCL(nc.GroupEnd());
-    for (int q = 0; q < n; ++q)
-      if (q != root)
-        TF_CUDA(tfb::cores_launch(d_out, W, H, g.tiles.as<TileDesc>(), nt, q, n, g.offs.as<int64_t>(),
-                                  g.recv.as<uint8_t>() + base[static_cast<size_t>(q)], true,
-                                  pl.max_core, s));
-  } else {
-    const size_t sz = static_cast<size_t>(size[static_cast<size_t>(ctx->rank)]);
-    TF_CUDA(g.packed.ensure(std::max<size_t>(sz, 1)));
-    TF_CUDA(tfb::cores_launch(d_out, W, H, g.tiles.as<TileDesc>(), nt, ctx->rank, n,
-                              g.offs.as<int64_t>(), g.packed.as<uint8_t>(), false, pl.max_core, s));
-    if (sz) TF_NCCL(nc.Send(g.packed.p, sz, ncclUint8, root, ctx->rank_comm, s));
-  }
-  return TF_OK;
+  return gather_cores(ctx, g, d_out, W, H, frames, tiles, root, s);
 }
 
 }  // extern "C"

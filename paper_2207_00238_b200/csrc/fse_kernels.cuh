@@ -14,6 +14,7 @@ struct TileDesc {
   int32_t cx, cy, cw, ch;  // core
   int32_t gw, gh;          // block-grid dims: ceil(hw/B), ceil(hh/B)
   int32_t grid_off;        // prefix sum of gw*gh over previous tiles
+  int32_t owner;           // part (GPU / rank) that reconstructs this unit (host LPT plan)
 };
 
 // One processed block: tile index + block-grid coordinates.
@@ -85,7 +86,7 @@ struct EnumLaunch {
   int32_t W, H, B;
   const TileDesc* tiles;
   int32_t n_tiles;
-  int32_t part, n_parts;      // only tiles t % n_parts == part are enqueued
+  int32_t part, n_parts;      // only tiles with owner == part are enqueued
   BlockDesc* blocks;          // out: blocks for the CTA kernel
   int32_t* n_blocks;          // out: their count
   unsigned long long* ref_blocks;  // out, per tile: blocks the reference processes

@@ -56,6 +56,27 @@ def test_synth_generator_is_deterministic_and_matches_config_shapes():
     assert all(c.min() == c.max() for c in cells)
 
 
+def lpt_owners(cost, parts):
+    """LPT restated: units by cost descending (ties: lower index first), each to the least
+    loaded part (ties: lowest part) -- capi.cpp assign_owners."""
+    order = sorted(range(len(cost)), key=lambda i: (-int(cost[i]), i))
+    load = [0] * parts
+    own = [0] * len(cost)
+    for u in order:
+        q = min(range(parts), key=lambda j: (load[j], j))
+        own[u] = q
+        load[q] += int(cost[u])
+    return own
+
+
+def test_core_layout_lpt_equal_costs_is_round_robin():
+    """Equal core areas (c3: 8 tiles of 960x1080) give the reference's i mod n (runtime.hpp:102)."""
+    for parts in (1, 2, 4, 8):
+        own = np.zeros(8, np.int32)
+        N.check(N.lib().tf_core_layout(3840, 2160, 1, 8, parts, None, None, own.ctypes.data, None, None))
+        assert list(own) == [t % parts for t in range(8)]
+
+
 def test_core_layout_partitions_every_tile_once():
     for frames, tiles, parts in ((1, 4, 1), (2, 4, 3), (3, 6, 8)):
         n = frames * tiles
@@ -66,8 +87,10 @@ def test_core_layout_partitions_every_tile_once():
         pb = np.zeros(parts, np.int64)
         N.check(N.lib().tf_core_layout(64, 48, frames, tiles, parts, cores, fr.ctypes.data,
                                        own.ctypes.data, offs.ctypes.data, pb.ctypes.data))
-        assert list(own) == [t % parts for t in range(n)]
         area = np.array([c.w * c.h for c in cores])
+        assert list(own) == lpt_owners(area, parts)
+        load = np.bincount(own, weights=area, minlength=parts)
+        assert load.max() - load.min() <= area.max()  # LPT balance bound
         assert pb.sum() == 64 * 48 * frames
         for p in range(parts):
             sel = np.where(own == p)[0]

@@ -1,7 +1,7 @@
 """World-size-2 CPU (gloo) tests of the multi-rank host logic.
 
-On the GPU path every rank runs the FSE for the tiles it owns
-(t % n_ranks == rank, runtime.hpp:102), packs their cores with the layout of
+On the GPU path every rank runs the FSE for the (frame, tile) units it owns
+(LPT on core pixels, tf_core_layout; replaces i mod n of runtime.hpp:102), packs their cores with the layout of
 tf_core_layout and NCCL-gathers them to rank 0, which unpacks them.  Here the
 same host-side layout and ownership are exercised over gloo; the per-tile FSE
 results come from the CPU oracle (test scaffolding standing in for the GPU;

@@ -140,3 +140,28 @@ def test_diffusion_restatement_equals_compiled_reference():
     for tiles, d, k in ((1, 0, 32), (4, 32, 32), (6, 8, 20), (3, 40, 5)):
         assert np.array_equal(O.tiled_diffusion(img, kn, tiles, d, k),
                               O.ref_run_local_diffusion(img, kn, tiles, d, k, 2))
+
+
+@needs_ref
+@pytest.mark.parametrize("cfg,W,H", [(1, 512, 512), (2, 640, 360), (3, 960, 540), (4, 800, 450), (5, 480, 270)])
+def test_reference_shim_generator_equals_product_generator(cfg, W, H):
+    """bench.py's reference arm builds its inputs with ref_synth_frame (synth_gen.hpp compiled
+    into oracle/_ref) so that it never loads the product library; the bytes must equal the
+    product's tf_synth_frame (the same header-only source)."""
+    from paper_2207_00238_b200 import tframe as T
+    for frame in (0, 3):
+        a = O.ref_synth_frame(cfg, frame, W, H)
+        b = T.synth_frame(cfg, frame, W, H)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@needs_ref
+def test_allcores_part_split_composes():
+    """The bounded-sample split of the reference arm (tiles t % n == part) covers every core."""
+    img, kn = O.ref_synth_frame(3, 0, 320, 200)
+    args = (8, 6, 4, 6, 20, 0.5, 0.7)
+    whole = O.ref_tiled_allcores(img, kn, *args, threads=4)
+    out = img.copy()
+    for part in range(3):
+        O.ref_tiled_allcores(img, kn, *args, threads=4, out=out, part=part, n_parts=3)
+    assert np.array_equal(out, whole)
