@@ -136,16 +136,18 @@ def ref_frames(wl):
     return np.stack(imgs), np.stack(kns)
 
 
+def band_blocks(wl, threads):
+    """Rows per task of the all-cores band split, in blocks: ~64-row bands (each band re-runs
+    a ceil(margin/B)*B-row apron above and below, so 1-block bands of small blocks would
+    repeat most of the work), fewer when the frame has too few rows to feed every thread."""
+    B = wl.params.block_size
+    return max(1, min(max(1, 64 // B), (wl.H * wl.frames) // (B * threads)))
+
+
 def ref_args(wl):
     p = wl.params
     return (wl.tiles, wl.overlap, p.block_size, p.support_margin, p.model_iterations,
             p.compensation, p.weight_decay)
-
-
-def core_pixels(wl, part, n_parts):
-    from paper_2207_00238_b200.tframe import plan_proposed  # pure host tiling (no GPU)
-    cores = plan_proposed(wl.W, wl.H, wl.tiles)
-    return sum(c[2] * c[3] for t, c in enumerate(cores) if t % n_parts == part) * wl.frames
 
 
 def ref_core_pixels(wl, part, n_parts):
@@ -172,7 +174,8 @@ def run_reference(args, wl, rank, world):
     for i in range(warmup + args.steps):
         part = i % n_sample
         t0 = time.perf_counter()
-        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, out=out, part=part, n_parts=n_sample)
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads),
+                             out=out, part=part, n_parts=n_sample)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -496,7 +499,8 @@ def cpu_baseline(wl, img_np, kn_np, ex_out, fa_out, parity):
         img, kn = img_np[:frames], kn_np[:frames]
         out = img.copy()
         t0 = time.perf_counter()
-        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, out=out, part=part, n_parts=n_parts)
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads),
+                             out=out, part=part, n_parts=n_parts)
         dt = time.perf_counter() - t0
         from dataclasses import replace
         pix = ref_core_pixels(replace(wl, frames=frames), part, n_parts)

@@ -403,7 +403,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // (within +-1 of EXACT / kernel ms): 0.99932 / 11.7, 0.99986 / 14.8, 0.99994 / 15.9 (the
   // CTA kernel: 1.0 / 24.6); 1 is the default: the FP32 weights' DFT is the main error source
   int wide = 0, wide_smem = 0;
-  int w64 = 1;
+  int w64 = 2;  // FP64 throughout
   if (const char* e = std::getenv("TF_WIDE_WM")) w64 = std::min(2, std::max(0, std::atoi(e)));
   if (!nowarp && !exact && !wkind && tfb::wide_supported(span) && !std::getenv("TF_NO_WIDE")) {
     const tfb::WideLayout wl(span, p.iters, w64);

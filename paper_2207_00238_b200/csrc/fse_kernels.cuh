@@ -171,7 +171,7 @@ struct WarpLayout {
 #define TF_HALF_T2 1  // 32x32 half kernel: y-transform on the 17 half rows first, then x
 #endif
 #ifndef TF_HALF_W32
-#define TF_HALF_W32 3  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 + FP32 rank-2 correction; 3: as 2 in packed FP32x2
+#define TF_HALF_W32 0  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 + FP32 rank-2 correction; 3: as 2 in packed FP32x2
 #endif
 #ifndef TF_HALF_ACC32
 #define TF_HALF_ACC32 0  // 1: FP32 correction accumulators + FP32 keys, FP64 R refreshed periodically
@@ -252,8 +252,8 @@ struct PairLayout {
   int region, off_log, log_stride, off_tw, total;
   __host__ __device__ PairLayout(int S, int iters) {
     const int hr = S / 2 + 1;
-    int r = 8 * S * (S + hr);
-    const int stage = 12 * S * S, cx = 24 * hr * S;
+    int r = 16 * S * (S + hr);                          // W rows 0..S-1 + copy of rows 0..hr-1 (FP64)
+    const int stage = 16 * S * S, cx = 32 * hr * S;     // staging (w, w v); C(x, l) of both
     r = r > stage ? r : stage;
     r = r > cx ? r : cx;
     region = (r + 15) & ~15;
