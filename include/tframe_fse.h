@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TF_ABI_VERSION 1
+#define TF_ABI_VERSION 2
 
 typedef enum tf_status {
   TF_OK = 0,
@@ -97,6 +97,8 @@ typedef struct tf_run_stats {
   int64_t pixels_evaluated;/* unknown core pixels written by the model        */
   double flops_executed;   /* FP64 flops the kernels actually execute (differs
                               from `flops` for the FAST half-spectrum kernel)  */
+  int64_t blocks_refined;  /* FAST: blocks whose greedy selection met an argmax
+                              near-tie and were re-run by the EXACT kernel     */
 } tf_run_stats;
 
 typedef struct tf_ctx tf_ctx;

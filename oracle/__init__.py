@@ -34,7 +34,8 @@ class orc_params(C.Structure):
 class orc_block_stats(C.Structure):
     _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("M", C.c_int32), ("L", C.c_int32),
                 ("iters", C.c_int32), ("pairs", C.c_int32), ("touched", C.c_int32),
-                ("unknown", C.c_int32), ("min_gap", C.c_double)]
+                ("unknown", C.c_int32), ("min_gap", C.c_double),
+                ("gap_iter", C.c_int32), ("pad", C.c_int32)]
 
 
 _orc = None

@@ -225,6 +225,7 @@ static void fit(model_t* md, const double* weights, const double* values, const 
     st->iters = 0;
     st->pairs = 0;
     st->min_gap = INFINITY;
+    st->gap_iter = -1;
   }
   if (wsum <= 0.0) return;
   for (int it = 0; it < p->iters; ++it) {
@@ -251,7 +252,10 @@ static void fit(model_t* md, const double* weights, const double* values, const 
         if (m > second) second = m;
       }
       const double gap = (best_mag - second) / best_mag;
-      if (gap < st->min_gap) st->min_gap = gap;
+      if (gap < st->min_gap) {
+        st->min_gap = gap;
+        st->gap_iter = it;
+      }
     }
     const double cr = (p->gamma * md->R_re[best]) / wsum;
     const double ci = (p->gamma * md->R_im[best]) / wsum;

@@ -23,6 +23,8 @@ typedef struct {
   int32_t touched;    /* touched bins T_b */
   int32_t unknown;    /* unknown pixels U_b */
   double min_gap;     /* min relative |R|^2 gap winner vs runner-up (divergence diagnostics) */
+  int32_t gap_iter;   /* iteration of that minimum (-1: none) */
+  int32_t pad;
 } orc_block_stats;
 
 int orc_plan_proposed(int W, int H, int N, int32_t* out_rects);

@@ -34,7 +34,7 @@ class tf_run_stats(C.Structure):
                 ("blocks_reference", C.c_int64), ("blocks_processed", C.c_int64),
                 ("kernel_ms", C.c_double), ("flops", C.c_double),
                 ("iterations", C.c_int64), ("pixels_evaluated", C.c_int64),
-                ("flops_executed", C.c_double)]
+                ("flops_executed", C.c_double), ("blocks_refined", C.c_int64)]
 
 
 class tf_quality_metrics(C.Structure):

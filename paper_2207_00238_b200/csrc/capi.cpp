@@ -117,6 +117,7 @@ struct Gpu {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_tables = nullptr;
   DevBuf img, known, out;                       // host-API frame buffers
   DevBuf tiles, blocks, counters, refblk, stats, rho, tw, offs, packed, recv, xblocks;
+  DevBuf tblocks;  // FAST blocks that met an argmax near-tie, re-run by the EXACT kernel
   DevBuf qbuf;                                  // quality metrics: sums, SSIM partials
   void* pinned = nullptr;                       // host staging for tables
   size_t pinned_n = 0;
@@ -127,7 +128,7 @@ struct Gpu {
   int occ_smem[2][tfb::kNumCfgs] = {};
   int wocc[2][33] = {};       // warp-kernel occupancy per bins-per-lane variant
   int wocc_smem[2][33] = {};
-  bool fft_ok = false;        // c_fft32 uploaded on this device
+  bool tw16_ok = false;       // c_tw16 uploaded on this device
   int pair_occ = 0, pair_smem = 0;  // FAST pair kernel (16x16 windows)
   // CUDA graph of the device path: the second identical call (same buffers, shape, params,
   // stream, mode and tuning environment) is captured, later identical calls replay it
@@ -137,8 +138,8 @@ struct Gpu {
   cudaGraphExec_t hexec = nullptr;
   std::string hkey, hlast;
   cudaEvent_t ev_gstart = nullptr, ev_cout = nullptr;
-  int wide_occ[3][65] = {};    // FAST wide kernel occupancy per (precision variant, window side)
-  int wide_smem[3][65] = {};
+  int wide_occ[65] = {};       // FAST wide kernel occupancy per window side
+  int wide_smem[65] = {};
   // streamed host path: copy-in / copy-out streams, a second compute stream, band events
   static constexpr int kMaxBands = 16;
   cudaStream_t cin = nullptr, cout = nullptr;
@@ -171,8 +172,51 @@ struct Gpu {
 
 }  // namespace tfh
 
+namespace tfh {
+// Tuning / debugging switches from the environment, read once per context (tf_create) and
+// again by tf_set_mode -- never per call; part of every CUDA-graph key.
+//   TF_NO_GRAPH       no graph capture / replay of repeated identical calls
+//   TF_STREAM_BANDS   row bands of the streamed single-GPU host path (1 = one shot)
+//   TF_HYBRID, TF_HYBRID_RATIO  FAST hybrid thresholds (known fraction of the window;
+//                     known window pixels per unknown block pixel); TF_HYBRID=0 disables
+//   TF_NO_TIE_GUARD   FAST: no argmax near-tie refinement by the EXACT kernel
+//   TF_NO_PAIR, TF_NO_WIDE, TF_NO_GEN, TF_NO_WARP, TF_HALF_NT, TF_FORCE_BIG  kernel choice
+//   TF_VERBOSE, TF_KTIME, TF_PHASE_DUMP, TF_STREAM_DEBUG  diagnostics on stderr
+struct Tune {
+  bool no_graph = false, no_tie_guard = false, no_pair = false, no_wide = false, no_gen = false;
+  bool no_warp = false, force_big = false, verbose = false, ktime = false, phase_dump = false;
+  bool stream_debug = false;
+  int half_nt = 32, stream_bands = 0;        // 0: automatic
+  float hybrid = 0.05f, hybrid_ratio = 1.5f;
+  std::string key;
+  void read() {
+    const auto on = [](const char* v) { return std::getenv(v) != nullptr; };
+    no_graph = on("TF_NO_GRAPH");
+    no_tie_guard = on("TF_NO_TIE_GUARD");
+    no_pair = on("TF_NO_PAIR");
+    no_wide = on("TF_NO_WIDE");
+    no_gen = on("TF_NO_GEN");
+    no_warp = on("TF_NO_WARP");
+    force_big = on("TF_FORCE_BIG");
+    verbose = on("TF_VERBOSE");
+    ktime = on("TF_KTIME");
+    phase_dump = on("TF_PHASE_DUMP");
+    stream_debug = on("TF_STREAM_DEBUG");
+    half_nt = on("TF_HALF_NT") ? std::atoi(std::getenv("TF_HALF_NT")) : 32;
+    stream_bands = on("TF_STREAM_BANDS") ? std::atoi(std::getenv("TF_STREAM_BANDS")) : 0;
+    hybrid = on("TF_HYBRID") ? static_cast<float>(std::atof(std::getenv("TF_HYBRID"))) : 0.05f;
+    hybrid_ratio = on("TF_HYBRID_RATIO") ? static_cast<float>(std::atof(std::getenv("TF_HYBRID_RATIO"))) : 1.5f;
+    char kb[160];
+    std::snprintf(kb, sizeof(kb), "%d%d%d%d%d%d%d %d %d %a %a", no_tie_guard, no_pair, no_wide, no_gen, no_warp,
+                  force_big, ktime, half_nt, stream_bands, hybrid, hybrid_ratio);
+    key = kb;
+  }
+};
+}  // namespace tfh
+
 struct tf_ctx {
   std::vector<tfh::Gpu> gpus;
+  tfh::Tune tune;
   int mode = TF_MODE_EXACT;
   ncclComm_t rank_comm = nullptr;  // one-process-per-GPU communicator
   int nranks = 1, rank = 0;
@@ -229,9 +273,9 @@ static int upload_tables(Gpu& g, const tf_fse_params& p, int wmax, cudaStream_t 
   TF_CUDA(cudaMemcpyAsync(g.rho.p, rho.data(), n_rho * sizeof(double), cudaMemcpyHostToDevice, s));
   TF_CUDA(cudaMemcpyAsync(g.tw.p, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   TF_CUDA(cudaStreamSynchronize(s));  // pageable sources: keep them alive until copied
-  if (tw_n >= 32 && !g.fft_ok) {  // constant-memory FFT twiddles (per device, once)
-    TF_CUDA(tfb::fft_tables_upload(tw.data() + 2 * (32 * 31 / 2)));
-    g.fft_ok = true;
+  if (tw_n >= 16 && !g.tw16_ok) {  // pair kernel's constant-memory twiddles (per device, once)
+    TF_CUDA(tfb::tw16_upload(tw.data() + 2 * (16 * 15 / 2)));
+    g.tw16_ok = true;
   }
   g.rho_val = p.rho;
   g.rho_margin = p.margin;
@@ -327,7 +371,7 @@ static int make_plan(int W, int H, int frames, int n_tiles, int overlap, int B, 
 }
 
 struct DevRun {
-  int64_t ref_blocks = 0, processed = 0, iterations = 0, evaluated = 0;
+  int64_t ref_blocks = 0, processed = 0, iterations = 0, evaluated = 0, refined = 0;
   double kernel_ms = 0.0, flops = 0.0, flops_executed = 0.0;
 };
 
@@ -363,7 +407,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   const tfb::SmemLayout lay(nb, pl.wmax, p.iters, nt / 32, half ? pl.wmax * pl.wmax : nb);
   // windows or selection logs past the shared-memory kernels' capacity: every block of the
   // launch on the big-window kernel (global scratch; TF_FORCE_BIG=1 forces it, for tests)
-  bool big = cfg0 < 0 || lay.total > 227 * 1024 || std::getenv("TF_FORCE_BIG");
+  const tfh::Tune& tu = ctx->tune;
+  bool big = cfg0 < 0 || lay.total > 227 * 1024 || tu.force_big;
   if (!big && g.occ_smem[exact][cfg] != lay.total) {
     int occ = 0;
     TF_CUDA(tfb::fse_prepare(cfg, exact, lay.total, &occ));
@@ -381,13 +426,12 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   //  FAST:  fse_half_kernel (Hermitian half spectrum) for span in {8, 16, 32}, one or two
   //         warps per block (TF_HALF_NT=32|64 overrides the per-span default).
   const int span = p.block + 2 * p.margin;
-  const bool nowarp = std::getenv("TF_NO_WARP") || span > pl.wmax || big;
+  const bool nowarp = tu.no_warp || span > pl.wmax || big;
   int wbpt = 0, wkind = 0;  // 1 = exact warp kernel, 2 = FAST half-spectrum warp kernel
-  int hnt = 32;  // threads per block of the half-spectrum kernel (measured: 64 is slower)
-  if (const char* e = std::getenv("TF_HALF_NT")) hnt = std::atoi(e);
+  const int hnt = tu.half_nt;  // threads per block of the half-spectrum kernel (measured: 64 is slower)
   if (!nowarp && exact) {
     wbpt = tfb::pick_warp_bpt(span, span);
-    if (wbpt > 16 && !std::getenv("TF_FORCE_WARP")) wbpt = 0;
+    if (wbpt > 16) wbpt = 0;
     wkind = wbpt ? 1 : 0;
   } else if (!nowarp) {
     wbpt = tfb::pick_half_bpth(hnt, span, span);
@@ -398,23 +442,17 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   if (wbpt && (!wlay.fits(wn, pl.wmax, p.iters) || wlay.total > 227 * 1024)) wbpt = wkind = 0;
   // FAST, full windows wider than a warp (span in (32, 64]): the wide half-spectrum kernel
   // (TF_NO_WIDE=1 keeps them on the CTA kernel); border windows stay on the CTA kernel
-  // precision variant (TF_WIDE_WM = 0|1|2): 0 = FP32 weights' DFT, W and update; 1 = FP64
-  // weights' DFT, FP32 W and update; 2 = FP64 throughout.  Measured on the full c4 frame
-  // (within +-1 of EXACT / kernel ms): 0.99932 / 11.7, 0.99986 / 14.8, 0.99994 / 15.9 (the
-  // CTA kernel: 1.0 / 24.6); 1 is the default: the FP32 weights' DFT is the main error source
   int wide = 0, wide_smem = 0;
-  int w64 = 2;  // FP64 throughout
-  if (const char* e = std::getenv("TF_WIDE_WM")) w64 = std::min(2, std::max(0, std::atoi(e)));
-  if (!nowarp && !exact && !wkind && tfb::wide_supported(span) && !std::getenv("TF_NO_WIDE")) {
-    const tfb::WideLayout wl(span, p.iters, w64);
+  if (!nowarp && !exact && !wkind && tfb::wide_supported(span) && !tu.no_wide) {
+    const tfb::WideLayout wl(span, p.iters);
     if (wl.total <= 227 * 1024) {
-      if (g.wide_smem[w64][span] != wl.total) {
+      if (g.wide_smem[span] != wl.total) {
         int occ = 0;
-        TF_CUDA(tfb::fse_wide_prepare(span, w64, wl.total, &occ));
-        g.wide_occ[w64][span] = occ;
-        g.wide_smem[w64][span] = wl.total;
+        TF_CUDA(tfb::fse_wide_prepare(span, wl.total, &occ));
+        g.wide_occ[span] = occ;
+        g.wide_smem[span] = wl.total;
       }
-      if (g.wide_occ[w64][span] >= 1) {
+      if (g.wide_occ[span] >= 1) {
         wide = span;
         wide_smem = wl.total;
       }
@@ -438,7 +476,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   if (wbpt && g.wocc[exact][wbpt] < 1) wbpt = wkind = 0;
   // FAST: clamped border windows through the GEN half kernel instead of the CTA kernel
   int gbpth = 0;
-  if (wkind == 2 && !std::getenv("TF_NO_GEN")) {
+  if (wkind == 2 && !tu.no_gen) {
     gbpth = span / 2 + 1;
     const tfb::HalfLayout glay(32, span, gbpth, std::max(pl.wmax, 32), 32);
     if (20 * p.iters > glay.wbytes || glay.total > 227 * 1024) gbpth = 0;
@@ -454,7 +492,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // FAST 16x16 full windows: the pair kernel (two blocks per warp; TF_NO_PAIR=1 keeps the
   // one-block-per-warp half kernel)
   int pair = 0, pair_smem = 0;
-  if (wkind == 2 && hnt == 32 && tfb::pair_supported(span)) {
+  if (wkind == 2 && hnt == 32 && tfb::pair_supported(span) && !tu.no_pair) {
     const tfb::PairLayout prl(span, p.iters);
     if (prl.total <= 227 * 1024) {
       if (g.pair_smem != prl.total) {
@@ -469,13 +507,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       }
     }
   }
-  if (std::getenv("TF_VERBOSE"))
+  if (tu.verbose)
     std::fprintf(stderr,
                  "[tframe] cta cfg %dx%d smem %d occ %d | warp kind %d bpt %d smem %d occ %d | gen %d smem %d occ %d"
                  " | wide %d smem %d occ %d | big %d\n",
                  nt, tfb::kCfgs[cfg].bpt, lay.total, g.occ[exact][cfg], wkind, wbpt, wsmem,
                  wbpt ? g.wocc[exact][wbpt] : 0, gbpth, gsmem, gbpth ? g.gocc[gbpth] : 0, wide,
-                 wide_smem, wide ? g.wide_occ[w64][wide] : 0, big ? 1 : 0);
+                 wide_smem, wide ? g.wide_occ[wide] : 0, big ? 1 : 0);
   int rc = TF_OK;
   const size_t n_tiles = pl.tiles.size();
   if (bd.first) {
@@ -491,6 +529,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     TF_CUDA(g.blocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
     TF_CUDA(g.wblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
     TF_CUDA(g.xblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
+    TF_CUDA(g.tblocks.ensure(nslots * static_cast<size_t>(pl.cand_blocks) * sizeof(BlockDesc)));
     TF_CUDA(g.counters.ensure(nslots * tfb::kCounters * sizeof(int32_t)));
     TF_CUDA(g.refblk.ensure(nslots * n_tiles * sizeof(unsigned long long)));
     TF_CUDA(cudaMemcpyAsync(g.tiles.p, g.pinned, n_tiles * sizeof(TileDesc), cudaMemcpyHostToDevice, s));
@@ -503,6 +542,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   }
   int32_t* counters = g.counters.as<int32_t>() + tfb::kCounters * bslot;
   BlockDesc* xblocks = g.xblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
+  BlockDesc* tblocks = g.tblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   BlockDesc* blocks = g.blocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   BlockDesc* wblocks = g.wblocks.as<BlockDesc>() + bslot * static_cast<size_t>(pl.cand_blocks);
   if (want_stats) {
@@ -558,14 +598,12 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // window is almost empty of known pixels run on the EXACT kernel (config 5)
   float hyb = 0.f;
   if (!exact && cfgx >= 0) {
-    hyb = 0.05f;  // c5: every |d| > 1 pixel of pure FAST sits in a block below 0.05
-    if (const char* h = std::getenv("TF_HYBRID")) hyb = static_cast<float>(std::atof(h));
+    hyb = tu.hybrid;  // c5: every |d| > 1 pixel of pure FAST sits in a block below 0.05
   }
   e.hyb_frac = hyb;
   e.hyb_ratio = 0.f;
   if (hyb > 0.f) {
-    e.hyb_ratio = 1.5f;  // fuzz (tools/fuzz_parity.py, 400 random cases): 1 -> 0.99944, 1.5 -> 0.99993, 2 -> 0.99997 within +-1
-    if (const char* r = std::getenv("TF_HYBRID_RATIO")) e.hyb_ratio = static_cast<float>(std::atof(r));
+    e.hyb_ratio = tu.hybrid_ratio;  // round-1 fuzz: 1 -> 0.99944, 1.5 -> 0.99993, 2 -> 0.99997 within +-1
   }
   e.xblocks = xblocks;
   e.n_xblocks = counters + 4;
@@ -590,6 +628,25 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   a.tw = g.tw.as<double>();
   a.wmax = pl.wmax;
   a.stats = want_stats ? g.stats.as<BlockStat>() : nullptr;
+  // FAST conditioning guard: blocks whose greedy selection meets an argmax near-tie are
+  // handed to the EXACT kernel (tblocks, counters 6/7), launched after the FAST kernels
+  const bool guard = !exact && cfgx >= 0 && !tu.no_tie_guard;
+  a.xlist = guard ? tblocks : nullptr;
+  a.n_xlist = counters + 6;
+  const auto launch_t = [&](cudaStream_t st) -> int {
+    if (!guard) return TF_OK;
+    tfb::FseLaunch x = a;
+    x.blocks = tblocks;
+    x.n_blocks = counters + 6;
+    x.next_block = counters + 7;
+    x.stats = nullptr;  // their FAST pass is in the statistics
+    x.xlist = nullptr;
+    // near-ties are rare (none on the c1-c5 frames): one CTA per SM, most exit at once
+    const int xg = static_cast<int>(std::min<int64_t>(g.sms, std::max<int64_t>(cand, 1)));
+    TF_CUDA(tfb::fse_launch(cfgx, true, x, xg, xsmem, st));
+    ++g.kl;
+    return TF_OK;
+  };
   const auto launch_x = [&](cudaStream_t st) -> int {
     if (hyb <= 0.f) return TF_OK;
     tfb::FseLaunch x = a;
@@ -597,6 +654,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     x.n_blocks = counters + 4;
     x.next_block = counters + 5;
     x.stats = want_stats ? g.stats.as<BlockStat>() + 2 * static_cast<size_t>(pl.cand_blocks) : nullptr;
+    x.xlist = nullptr;
     const int xg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.occ[1][cfgx],
                                                       std::max<int64_t>(cand, 1)));
     TF_CUDA(tfb::fse_launch(cfgx, true, x, xg, xsmem, st));
@@ -618,23 +676,23 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // launches (c2 0.685 vs 0.720 ms after them), after them in the streamed path's bands
   // (launched first, each band's kernels waited for SM slots behind the other bands: c2 host
   // call 0.79 vs 0.83-0.86 ms); concurrently on a fork even an empty list cost 5-11 %
-  const bool x_first = std::getenv("TF_X_FIRST") ? std::atoi(std::getenv("TF_X_FIRST")) != 0 : !band;
+  const bool x_first = !band;
   if (x_first) {
     rc = launch_x(s);
     if (rc != TF_OK) return rc;
   }
-  const bool ktime = std::getenv("TF_KTIME") != nullptr;  // tuning aid: per-kernel split
+  const bool ktime = tu.ktime;  // tuning aid: per-kernel split
   if (wide) {
     // border windows (CTA kernel) on a forked stream, concurrently with the wide kernel
     TF_CUDA(cudaEventRecord(g.ev_fork, s));
     TF_CUDA(cudaStreamWaitEvent(side, g.ev_fork, 0));
-    const bool border_after = std::getenv("TF_GEN_BEFORE") ? false : !graph;  // as in the warp-kernel branch
+    const bool border_after = !graph;  // as in the warp-kernel branch
     if (!border_after) {
       TF_CUDA(tfb::fse_launch(cfg, exact, a, grid, lay.total, side));
       ++g.kl;
       TF_CUDA(cudaEventRecord(g.ev_join, side));
     }
-    const int wgrid = g.sms * g.wide_occ[w64][wide];
+    const int wgrid = g.sms * g.wide_occ[wide];
     const size_t per = static_cast<size_t>(wgrid) * p.iters;  // log entries per band slot
     TF_CUDA(g.wlog_kl.ensure(nslots * per * sizeof(int32_t)));
     TF_CUDA(g.wlog_c.ensure(nslots * per * sizeof(double2)));
@@ -645,7 +703,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     w.stats = want_stats ? g.stats.as<BlockStat>() + pl.cand_blocks : nullptr;
     w.wlog_kl = g.wlog_kl.as<int32_t>() + bslot * per;
     w.wlog_c = g.wlog_c.as<double2>() + bslot * per;
-    TF_CUDA(tfb::fse_wide_launch(wide, w64, w,
+    TF_CUDA(tfb::fse_wide_launch(wide, w,
                                  static_cast<int>(std::min<int64_t>(wgrid, std::max<int64_t>(cand, 1))),
                                  wide_smem, s));
     ++g.kl;
@@ -687,7 +745,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     // launches: main first, then the border kernel on the fork (the other order made c2
     // bimodal, 0.686 / 0.720 ms per process); in a captured graph the opposite capture order
     // gives that dispatch order (measured: 0.699 vs 0.731 ms per step)
-    const bool border_after = std::getenv("TF_GEN_BEFORE") ? false : !graph;
+    const bool border_after = !graph;
     if (!border_after) {
       rc = launch_border();
       if (rc != TF_OK) return rc;
@@ -740,6 +798,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     rc = launch_x(s);
     if (rc != TF_OK) return rc;
   }
+  rc = launch_t(s);
+  if (rc != TF_OK) return rc;
   if (ktime) {
     TF_CUDA(cudaStreamSynchronize(s));
     int32_t cnt[tfb::kCounters];
@@ -767,6 +827,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     for (size_t t = 0; t < n_tiles; ++t)
       if (pl.tiles[t].owner == part) res->ref_blocks += static_cast<int64_t>(ref[t]);
     res->processed = cnt[0] + cnt[2] + cnt[4];
+    res->refined = cnt[6];
     std::vector<BlockStat> st(static_cast<size_t>(cnt[0] + cnt[2] + cnt[4]));
     if (cnt[0] > 0)
       TF_CUDA(cudaMemcpy(st.data(), g.stats.p, static_cast<size_t>(cnt[0]) * sizeof(BlockStat),
@@ -824,7 +885,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     }
     res->flops = fl;
     res->flops_executed = xfl;
-    if (std::getenv("TF_PHASE_DUMP")) {  // tuning aid (TF_PHASE_TIMING builds)
+    if (tu.phase_dump) {  // tuning aid (TF_PHASE_TIMING builds)
       double c[4] = {0, 0, 0, 0};
       for (const BlockStat& b : st)
         for (int q = 0; q < 4; ++q) c[q] += b.cyc[q];
@@ -862,18 +923,6 @@ static int drop_graph(Gpu& g) {
   g.hkey.clear();
   g.hlast.clear();
   return TF_OK;
-}
-
-// Tuning environment that changes the enqueued work (part of every graph key).
-static std::string env_key() {
-  std::string key;
-  for (const char* v : {"TF_HYBRID", "TF_HYBRID_RATIO", "TF_X_FIRST", "TF_GEN_BEFORE", "TF_WIDE_WM", "TF_NO_PAIR", "TF_NO_WIDE", "TF_NO_GEN",
-                        "TF_NO_WARP", "TF_HALF_NT", "TF_FSE_CFG", "TF_FORCE_WARP", "TF_FORCE_BIG", "TF_STREAM_CHUNKS", "TF_STREAM_UNIFORM"}) {
-    const char* e = std::getenv(v);
-    key += e ? e : "-";
-    key += '|';
-  }
-  return key;
 }
 
 using clk = std::chrono::steady_clock;
@@ -985,6 +1034,7 @@ tf_ctx* tf_create(int n_gpus, const int* device_ids) {
     return nullptr;
   }
   auto ctx = std::make_unique<tf_ctx>();
+  ctx->tune.read();
   ctx->gpus.resize(static_cast<size_t>(n_gpus));
   for (int i = 0; i < n_gpus; ++i) {
     Gpu& g = ctx->gpus[static_cast<size_t>(i)];
@@ -1070,6 +1120,7 @@ int tf_set_mode(tf_ctx* ctx, int mode) {
   if (!ctx) return set_error(TF_EINVAL, "null context");
   if (mode != TF_MODE_EXACT && mode != TF_MODE_FAST) return set_error(TF_EINVAL, "bad mode");
   ctx->mode = mode;
+  ctx->tune.read();
   return TF_OK;
 }
 
@@ -1103,7 +1154,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
   if (cap != cudaStreamCaptureStatusNone)
     return set_error(TF_EINVAL, "stream is capturing a CUDA graph: call tf_tiled_extrapolate_device outside "
                                 "the capture (repeated identical calls replay the library's own graph)");
-  if (!stats && !std::getenv("TF_NO_GRAPH")) {
+  if (!stats && !ctx->tune.no_graph) {
     // graph path: identical repeated calls (the serving / benchmark loop) replay one CUDA
     // graph of the whole enqueue sequence, so the GPU runs it back to back without waiting
     // for ~10 host API calls per call
@@ -1111,7 +1162,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
     std::snprintf(kb, sizeof(kb), "%p %p %p %d %d %d %d %d %d %d %d %a %a %d %d %p %d|", d_img, d_known,
                   d_out, W, H, frames, tiles, overlap, p->block, p->margin, p->iters, p->gamma, p->rho,
                   part, n_parts, static_cast<void*>(s), ctx->mode);
-    const std::string key = std::string(kb) + env_key();
+    const std::string key = std::string(kb) + ctx->tune.key;
     const bool tables_ok = g.rho_val == p->rho && g.rho_margin == p->margin && g.tw_wmax >= pl.wmax;
     if (!(g.gexec && g.gkey == key) && g.last_key == key && tables_ok) {
       rc = drop_graph(g);  // one graph at a time: both read the pinned tile staging
@@ -1178,6 +1229,7 @@ int tf_tiled_extrapolate_device(tf_ctx* ctx, int gpu, const uint8_t* d_img, cons
     stats->overhead_pixels = pl.overhead;
     stats->blocks_reference = dr.ref_blocks;
     stats->blocks_processed = dr.processed;
+    stats->blocks_refined = dr.refined;
     stats->kernel_ms = dr.kernel_ms;
     stats->flops = dr.flops;
     stats->flops_executed = dr.flops_executed;
@@ -1208,11 +1260,10 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   // first, so bands complete roughly in order and their copy-out overlaps later bands
   int least = 0, greatest = 0;
   TF_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-  const bool prio = !std::getenv("TF_NO_BAND_PRIO");
   for (int k = 0; k < Gpu::kMaxBands; ++k) {
     if (!g.ev_in[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_in[k], cudaEventDisableTiming));
     if (!g.ev_done[k]) TF_CUDA(cudaEventCreateWithFlags(&g.ev_done[k], cudaEventDisableTiming));
-    const int pr = prio ? std::min(least, greatest + k) : least;
+    const int pr = std::min(least, greatest + k);
     if (g.bs[k] && g.bs_prio[k] != pr) {
       TF_CUDA(cudaStreamSynchronize(g.bs[k]));
       TF_CUDA(cudaStreamDestroy(g.bs[k]));
@@ -1236,7 +1287,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   // device-to-device copy on the copy-in stream would wait for SM slots behind the kernels)
   uint8_t* dout = di;
   // TF_STREAM_DEBUG: timing events (start, chunks, band starts / ends, copy-out end)
-  const bool dbg = !capture && std::getenv("TF_STREAM_DEBUG");
+  const bool dbg = !capture && ctx->tune.stream_debug;
   cudaEvent_t* dev_t = g.dbg_ev;
   if (dbg && !dev_t[0])
     for (cudaEvent_t& e : g.dbg_ev) TF_CUDA(cudaEventCreate(&e));
@@ -1264,15 +1315,14 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   // that needs them, so band 0's kernels are enqueued after only its own chunks.
   // chunks: a few large copies beat many small ones (each H2D has a fixed cost; c2
   // measured 0.79 ms per call with 2 bands / 3 chunks vs 0.81-0.85 with 8-12 chunks)
-  int nin = std::min(Gpu::kMaxBands, std::max(nb + 1, 3));
-  if (const char* e = std::getenv("TF_STREAM_CHUNKS")) nin = std::min(Gpu::kMaxBands, std::max(1, std::atoi(e)));
+  const int nin = std::min(Gpu::kMaxBands, std::max(nb + 1, 3));
   const int span = p.block + p.margin;  // rows a window reaches below its block's first row
   // chunk 0 ends exactly at the last row band 0's windows reach (band 0 starts as soon as
   // it can), the remaining rows in nin - 1 equal chunks (measured host call, vs nin equal
   // chunks, TF_STREAM_UNIFORM=1: c2 0.775 vs 0.790 ms, c3 5.80 vs 6.00, c4 12.94 vs 13.11)
   std::vector<int64_t> cb(static_cast<size_t>(nin) + 1, rows);
   cb[0] = 0;
-  if (!std::getenv("TF_STREAM_UNIFORM") && nin > 1) {
+  if (nin > 1) {
     cb[1] = std::min(rows, std::max<int64_t>(1, std::min(rows - 1, std::max<int64_t>(R - 1 + span, R)) + 1));
     const int64_t rest = (rows - cb[1] + nin - 2) / (nin - 1);
     for (int c = 2; c < nin; ++c) cb[static_cast<size_t>(c)] = std::min(rows, cb[1] + (c - 1) * rest);
@@ -1368,7 +1418,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
       std::fprintf(stderr, " %.0f/%.0f", at(1 + Gpu::kMaxBands + k), at(1 + 2 * Gpu::kMaxBands + k));
     std::fprintf(stderr, " | copy-out end %.0f\n", at(3 * Gpu::kMaxBands + 1));
   }
-  if (std::getenv("TF_STREAM_DEBUG")) {
+  if (ctx->tune.stream_debug) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, g.ev0, g.ev1);
     std::fprintf(stderr, "[tframe] streamed %d bands: enqueue %lld us, total %lld us, compute span %.1f us\n",
@@ -1492,7 +1542,7 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
     // ~25-35 us per band and banding adds ~5 % compute (smaller launches), so bands stay a
     // few hundred rows tall
     nbands = static_cast<int>(std::clamp<int64_t>(rows / 512, 1, 8));
-    if (const char* e = std::getenv("TF_STREAM_BANDS")) nbands = std::atoi(e);
+    if (ctx->tune.stream_bands > 0) nbands = ctx->tune.stream_bands;
     nbands = std::max(1, std::min(nbands, Gpu::kMaxBands));
     if ((rows + nbands - 1) / nbands < p->block) nbands = 1;  // a block spans at most 2 bands
   }
@@ -1512,13 +1562,13 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       return at.type == cudaMemoryTypeHost;
     };
     std::string key;
-    if (!std::getenv("TF_NO_GRAPH") && pinned(img) && pinned(known) && pinned(out)) {
+    if (!ctx->tune.no_graph && pinned(img) && pinned(known) && pinned(out)) {
       char kb[512];
       std::snprintf(kb, sizeof(kb), "%p %p %p %d %d %d %d %d %d %d %d %a %a %d %d|",
                     static_cast<const void*>(img), static_cast<const void*>(known),
                     static_cast<void*>(out), W, H, frames, tiles, overlap, p->block, p->margin,
                     p->iters, p->gamma, p->rho, ctx->mode, nbands);
-      key = std::string(kb) + env_key();
+      key = std::string(kb) + ctx->tune.key;
     }
     const bool tables_ok = g.rho_val == p->rho && g.rho_margin == p->margin && g.tw_wmax >= pl.wmax;
     if (!key.empty() && !(g.hexec && g.hkey == key) && g.hlast == key && tables_ok) {
@@ -1574,9 +1624,11 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       std::vector<unsigned long long> ref(pl.tiles.size() * static_cast<size_t>(nbands));
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));
-      for (int k = 0; k < nbands; ++k)
+      for (int k = 0; k < nbands; ++k) {
+        stats->blocks_refined += cnt[tfb::kCounters * k + 6];
         stats->blocks_processed += cnt[tfb::kCounters * k] + cnt[tfb::kCounters * k + 2] +
                                    cnt[tfb::kCounters * k + 4];
+      }
       for (unsigned long long r : ref) stats->blocks_reference += static_cast<int64_t>(r);
     }
     return TF_OK;
@@ -1631,6 +1683,7 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
       int32_t cnt[tfb::kCounters];
       TF_CUDA(cudaMemcpy(cnt, g.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
       stats->blocks_processed += cnt[0] + cnt[2] + cnt[4];
+      stats->blocks_refined += cnt[6];
       std::vector<unsigned long long> ref(pl.tiles.size());
       TF_CUDA(cudaMemcpy(ref.data(), g.refblk.p, ref.size() * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));

@@ -54,6 +54,10 @@ struct FseLaunch {
   double2* wlog_c;
   unsigned char* scratch;  // big-window kernel: per-CTA spectra and model (BigLayout bytes each)
   int32_t nmax;            // big-window kernel: largest support window (bins) of the launch
+  // FAST kernels: blocks whose greedy selection met an argmax near-tie are appended here
+  // (and not evaluated); the EXACT kernel re-runs them afterwards (nullptr: no guard)
+  BlockDesc* xlist;
+  int32_t* n_xlist;
 };
 
 // Big-window kernel (windows past the shared-memory kernels' capacity, or selection logs too
@@ -170,16 +174,7 @@ struct WarpLayout {
 #ifndef TF_HALF_T2
 #define TF_HALF_T2 1  // 32x32 half kernel: y-transform on the 17 half rows first, then x
 #endif
-#ifndef TF_HALF_W32
-#define TF_HALF_W32 0  // 0: W FP64; 1: W FP32 (8 B), FP64 math; 2: W FP32 + FP32 rank-2 correction; 3: as 2 in packed FP32x2
-#endif
-#ifndef TF_HALF_ACC32
-#define TF_HALF_ACC32 0  // 1: FP32 correction accumulators + FP32 keys, FP64 R refreshed periodically
-#endif
-#ifndef TF_HALF_REFRESH
-#define TF_HALF_REFRESH 8  // iterations between FP64 refreshes (power of two)
-#endif
-constexpr int kHalfWB = (TF_HALF_W32 || TF_HALF_ACC32) ? 8 : 16;  // bytes per W element
+constexpr int kHalfWB = 16;  // bytes per W element (binary64 complex)
 
 // Windows up to 16 x 16 (one warp, <= 5 rows per lane) keep the selection log in shared
 // memory (after the sync area) instead of a global scratch: short loops, where the per-
@@ -195,12 +190,12 @@ struct HalfLayout {
     const int lmax = bpth * (nt / M) - 1;
     const int rows = kHalfWB * M * (L + lmax + 1);
     int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
-    if (nt == 32 && M == L && scratch < 24 * bpth * 32)
-      scratch = 24 * bpth * 32;  // TF_HALF_T2: C(x, l) of the half rows, FP64 values + FP32 weights
+    if (nt == 32 && M == L && scratch < 32 * bpth * 32)
+      scratch = 32 * bpth * 32;  // TF_HALF_T2: C(x, l) of the half rows, values + weights (FP64)
     wbytes = (rows > scratch ? rows : scratch);
     wbytes = (wbytes + 15) & ~15;
     off_tw = wbytes;
-    off_sync = off_tw + 32 * wmax + 32 * wmax;  // FP64 twiddles x/y, FP32 x/y/y-swapped/x-swapped
+    off_sync = off_tw + 32 * wmax;  // twiddles x / y (FP64 complex)
     total = off_sync + 4 * 32 + 16;  // argmax slots (two warps), block id, sum of weights
     off_log = (total + 15) & ~15;
     if (log_iters > 0) total = off_log + 20 * log_iters;
@@ -216,29 +211,23 @@ struct HalfLayout {
 //   [twiddles: FP64 (cos, sin) x S, FP32 (cos, -sin) x S, FP32 (sin, cos) x S][slots][misc]
 struct WideLayout {
   int nt, g, hr, bp, rows, region, off_tw, off_slots, off_misc, total;
-#ifndef TF_WIDE_NT1
-#define TF_WIDE_NT1 96  // threads per block of the FP64-DFT (WM1) variant for S <= 48 (192: c4 13.3 vs 12.1 ms)
-#endif
-  __host__ __device__ static constexpr int threads(int S, int wm) {
-    return wm == 2 ? (S <= 48 ? 192 : 256) : wm == 1 ? (S <= 48 ? TF_WIDE_NT1 : 256) : (S <= 48 ? 96 : 128);
-  }
-  __host__ __device__ WideLayout(int S, int iters, int wm) {
-    nt = threads(S, wm);
+  __host__ __device__ static constexpr int threads(int S) { return S <= 48 ? 192 : 256; }
+  __host__ __device__ WideLayout(int S, int iters) {
+    nt = threads(S);
     g = nt / S;
     hr = S / 2 + 1;
     bp = (hr + g - 1) / g;
     rows = S + hr + g;
-    const int eb = wm == 2 ? 16 : 8;
-    int r = eb * S * rows;                   // W, copy rows included
-    const int stage = (wm ? 16 : 12) * S * S;  // w + w*v per window pixel
-    const int cx = (wm ? 32 : 24) * hr * S;    // C(x, l): values double2 + weights
-    const int lg = 20 * iters;               // selection log (double2 + int32 per iteration)
+    int r = 16 * S * rows;        // W (binary64 complex), copy rows included
+    const int stage = 16 * S * S;  // w + w*v per window pixel
+    const int cx = 32 * hr * S;    // C(x, l): values + weights
+    const int lg = 20 * iters;     // selection log (double2 + int32 per iteration)
     r = r > stage ? r : stage;
     r = r > cx ? r : cx;
     r = r > lg ? r : lg;
     region = (r + 15) & ~15;
     off_tw = region;
-    off_slots = off_tw + 32 * S;
+    off_slots = off_tw + 16 * S;
     off_misc = off_slots + 2 * (nt / 32) * 32;
     total = off_misc + 16;
   }
@@ -285,7 +274,7 @@ cudaError_t diffusion_launch(const uint8_t* img, const uint8_t* known, uint8_t* 
                              int iters, double* f0, double* f1, cudaStream_t s);
 
 // FFT twiddles (constant memory) from the size-32 cos/sin table: 32 x (cos, sin) of 2 pi j / 32
-cudaError_t fft_tables_upload(const double* tw32);
+cudaError_t tw16_upload(const double* tw16);  // pair kernel's constant twiddles (16-point)
 cudaError_t div_selftest_launch(long long n, unsigned long long seed, unsigned long long* bad,
                                 cudaStream_t s);
 // warp kernel variants: bins per lane (window M*L = 32*bpt with 32 % M == 0)
@@ -300,9 +289,8 @@ cudaError_t fse_half_launch(int nt, int bpth, const FseLaunch& a, int grid, int 
                                  cudaStream_t s);
 // FAST wide kernel for full S x S windows, S in {40, 44, 48, 56, 64} (0 = no variant)
 int wide_supported(int S);
-cudaError_t fse_wide_prepare(int S, int wm, int smem_bytes, int* ctas_per_sm);
-cudaError_t fse_wide_launch(int S, int wm, const FseLaunch& a, int grid, int smem_bytes,
-                            cudaStream_t s);
+cudaError_t fse_wide_prepare(int S, int smem_bytes, int* ctas_per_sm);
+cudaError_t fse_wide_launch(int S, const FseLaunch& a, int grid, int smem_bytes, cudaStream_t s);
 // Quality metrics (metrics.cu): per frame sse3[3f..3f+2] = {sum d^2, sum over unknown d^2,
 // unknown count} (known may be null); with partial (ssim_partials doubles) and ssim_sum
 // (frames doubles), the per-frame sum of the 8x8 window SSIM values.

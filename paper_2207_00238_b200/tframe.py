@@ -159,6 +159,10 @@ class Context:
         check(lib().tf_set_mode(self._h, m))
         self.mode = mode
 
+    def reload_tuning(self) -> None:
+        """Re-read the TF_* tuning environment (read once per context, include/tframe_fse.h)."""
+        check(lib().tf_set_mode(self._h, {"exact": N.TF_MODE_EXACT, "fast": N.TF_MODE_FAST}[self.mode]))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().tf_destroy(self._h)
@@ -474,13 +478,14 @@ class RunStats:
     iterations: int = 0
     pixels_evaluated: int = 0
     flops_executed: float = 0.0
+    blocks_refined: int = 0
     tiles: list = field(default_factory=list)
 
     @classmethod
     def _from_c(cls, s: N.tf_run_stats) -> "RunStats":
         return cls(s.plan_us, s.distribute_us, s.compute_span_us, s.merge_us, s.total_us,
                    s.overhead_pixels, s.blocks_reference, s.blocks_processed, s.kernel_ms,
-                   s.flops, s.iterations, s.pixels_evaluated, s.flops_executed)
+                   s.flops, s.iterations, s.pixels_evaluated, s.flops_executed, s.blocks_refined)
 
 
 def run_master(image: np.ndarray, mask: np.ndarray, config: MasterConfig,

@@ -23,3 +23,27 @@ def _built():
     build.build_oracle(with_ref=Path(os.environ.get("TF_REF_INCLUDE", "/root/reference/proj/include")).exists()
                        and not (ROOT / "oracle" / "_ref" / "libtframe_ref.so").exists())
     yield
+
+
+@pytest.fixture
+def tune_env(monkeypatch):
+    """Set tuning variables (TF_STREAM_BANDS, TF_HYBRID, ...) for some contexts: the library
+    reads them once per context (tf_create / tf_set_mode), so the contexts re-read them
+    (Context.reload_tuning) now and again after the environment is restored."""
+    touched = []
+
+    def set_env(ctxs, **env):
+        for k, v in env.items():
+            if v is None:
+                monkeypatch.delenv(k, raising=False)
+            else:
+                monkeypatch.setenv(k, str(v))
+        for c in ctxs:
+            c.reload_tuning()
+            touched.append(c)
+
+    yield set_env
+    monkeypatch.undo()
+    for c in touched:
+        if c._h:
+            c.reload_tuning()

@@ -24,7 +24,7 @@ def test_every_declared_symbol_is_exported_and_bound():
         assert hasattr(L, n), f"{n} not exported"
         assert n in N.SIGNATURES, f"{n} has no ctypes signature"
     assert set(N.SIGNATURES) == set(names)
-    assert L.tf_abi_version() == 1
+    assert L.tf_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu():

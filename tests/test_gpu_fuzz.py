@@ -1,8 +1,10 @@
-"""Randomised parity sweep on the GPU (tools/fuzz_parity.py): random shapes, block sizes
-2-16, margins 0-16, iterations, gamma, rho, tiles, overlap, frames and four mask families
-(i.i.d. pixels, aligned cells, disks, almost nothing known).  EXACT must equal the C oracle
-byte for byte and match its block counts in every case; FAST (with its EXACT hybrid) must
-keep >= 99.9 % of the reconstructed pixels within +-1 of EXACT over the sweep."""
+"""Randomised parity sweep on the GPU (tools/fuzz_parity.py): 400 random cases over shape,
+block sizes 2-16, margins 0-16, iterations, gamma, rho, tiles, overlap, frames and six mask
+families (i.i.d. pixels, aligned cells, disks, almost nothing known, cell losses with
+margins 0-2, scratch lines).  EXACT must equal the C oracle byte for byte and match its
+block counts in every case; FAST must meet the north-star tolerance in EVERY case (>= 99.9 %
+of the reconstructed pixels within +-1 of EXACT, |dPSNR vs the truth| <= 0.05 dB); cases
+where FAST differs at all carry an argmax-gap report (asserted to be present)."""
 import importlib.util
 from pathlib import Path
 
@@ -19,14 +21,21 @@ def _fuzz():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", [101, 202])
+@pytest.mark.parametrize("seed", [101, 202, 303, 404])
 def test_randomised_parity_sweep(seed):
     from paper_2207_00238_b200 import tframe as T
+    fz = _fuzz()
     ex, fa = T.Context(1, [0], "exact"), T.Context(1, [0], "fast")
     try:
-        bad, within1 = _fuzz().run(60, seed, ex, fa, verbose=False)
+        recs = fz.run(100, seed, ex, fa, verbose=False)
     finally:
         ex.close()
         fa.close()
-    assert bad == 0
-    assert within1 >= 0.999, within1
+    assert len(recs) >= 90
+    bad = [r for r in recs if not r["exact_ok"]]
+    assert not bad, bad[:3]
+    off = [r for r in recs if r["within1"] < fz.WITHIN1 or r["dpsnr"] > fz.DPSNR_DB]
+    assert not off, [(r["within1"], r["dpsnr"], r["params"], r["divergences"][:2]) for r in off[:3]]
+    for r in recs:
+        if r["n_diff"]:
+            assert r["divergences"], r  # every difference is attributed to a block

@@ -155,7 +155,7 @@ def test_device_calls_on_two_streams_back_to_back(mode):
         ctx.close()
 
 
-def test_streamed_bands_on_the_big_window_kernel(monkeypatch):
+def test_streamed_bands_on_the_big_window_kernel(tune_env):
     """640x1080, B = 64, margin = 64 (192x192 windows, big-window kernel) in 2 concurrent
     bands with different candidate counts: byte-identical to one shot and to the oracle."""
     W, H, B, m, I = 640, 1080, 64, 64, 6
@@ -171,9 +171,9 @@ def test_streamed_bands_on_the_big_window_kernel(monkeypatch):
     for mode in ("exact", "fast"):
         ctx = T.Context(1, [0], mode)
         try:
-            monkeypatch.setenv("TF_STREAM_BANDS", "1")
+            tune_env([ctx], TF_STREAM_BANDS=1)
             one, _ = ctx.tiled(img, kn, 1, 0, p)
-            monkeypatch.setenv("TF_STREAM_BANDS", "2")
+            tune_env([ctx], TF_STREAM_BANDS=2)
             for _ in range(3):
                 got, _ = ctx.tiled(img, kn, 1, 0, p)
                 assert np.array_equal(got, one), f"{mode}: {(got != one).sum()} px differ"

@@ -116,12 +116,12 @@ def test_fast_mode_within_tolerance(ctx, fctx):
 
 
 @pytest.mark.parametrize("no_gen", [False, True])
-def test_fast_mode_border_windows(ctx, fctx, no_gen, monkeypatch):
+def test_fast_mode_border_windows(ctx, fctx, no_gen, tune_env):
     """Small, odd-sized frames: most windows are clamped by the halo (M, L not powers of two),
     which the FAST path runs through the GEN half-spectrum warp kernel, or (TF_NO_GEN=1)
     through the half-spectrum CTA kernel."""
     if no_gen:
-        monkeypatch.setenv("TF_NO_GEN", "1")
+        tune_env([fctx], TF_NO_GEN=1)
     ds = []
     for cfg in (2, 3):
         wl = CONFIGS[cfg]
@@ -256,7 +256,7 @@ def test_exact_mode_full_config_frame_equals_reference(ctx, cfg):
 
 
 @pytest.mark.parametrize("cfg,frames", [(2, 1), (3, 1), (5, 3), (1, 1)])
-def test_streamed_host_path_equals_one_shot(ctx, fctx, cfg, frames, monkeypatch):
+def test_streamed_host_path_equals_one_shot(ctx, fctx, cfg, frames, tune_env):
     """The single-GPU host path streams row bands (H2D / FSE / D2H overlap over streams); its
     output and block counts must equal the one-shot path (TF_STREAM_BANDS=1) for any band
     count, in both modes, including multi-frame batches."""
@@ -267,10 +267,10 @@ def test_streamed_host_path_equals_one_shot(ctx, fctx, cfg, frames, monkeypatch)
     img = np.stack(imgs) if frames > 1 else imgs[0]
     kn = np.stack(kns) if frames > 1 else kns[0]
     for c in (ctx, fctx):
-        monkeypatch.setenv("TF_STREAM_BANDS", "1")
+        tune_env([c], TF_STREAM_BANDS=1)
         want, st1 = c.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
         for nb in ("2", "5", "8", "16"):
-            monkeypatch.setenv("TF_STREAM_BANDS", nb)
+            tune_env([c], TF_STREAM_BANDS=nb)
             got, st = c.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
             assert np.array_equal(got, want), f"c{cfg} {c.mode} bands={nb}: {(got != want).sum()} pixels differ"
             assert st.blocks_processed == st1.blocks_processed
@@ -306,7 +306,7 @@ def test_fast_kernels_with_empty_windows_and_odd_block_counts(ctx, fctx, cfg):
     assert (fa == 128).all()
 
 
-def test_fast_hybrid_routes_ill_conditioned_blocks(ctx, fctx, monkeypatch):
+def test_fast_hybrid_routes_ill_conditioned_blocks(ctx, fctx, tune_env):
     """Config 5 frames: with the hybrid off (TF_HYBRID=0) FAST leaves the tolerance; with it on
     the blocks it routes to the EXACT kernel are counted in blocks_processed and the output
     meets the tolerance; EXACT mode ignores the setting."""
@@ -315,9 +315,9 @@ def test_fast_hybrid_routes_ill_conditioned_blocks(ctx, fctx, monkeypatch):
     img, kn = np.stack(imgs), np.stack(kns)
     ex, st_e = ctx.tiled(img, kn, 1, wl.overlap, wl.params)
     unk = kn == 0
-    monkeypatch.setenv("TF_HYBRID", "0")
+    tune_env([fctx, ctx], TF_HYBRID=0, TF_NO_TIE_GUARD=1)
     fa0, _ = fctx.tiled(img, kn, 1, wl.overlap, wl.params)
-    monkeypatch.setenv("TF_HYBRID", "0.05")
+    tune_env([fctx, ctx], TF_HYBRID=0.05, TF_NO_TIE_GUARD=None)
     fa1, st_f = fctx.tiled(img, kn, 1, wl.overlap, wl.params)
     ex1, _ = ctx.tiled(img, kn, 1, wl.overlap, wl.params)
     assert np.array_equal(ex, ex1)
@@ -416,7 +416,7 @@ def test_gpu_reproduces_reference_golden_fixtures(ctx, fctx, name):
     unk = d["known"] == 0
     if unk.any():
         dd = np.abs(fa.astype(int) - d["out"].astype(int))[unk]
-        assert (dd <= 1).mean() >= FAST_WITHIN1 or dd.size < 1000 and (dd <= 1).mean() >= 0.99, name
+        assert (dd <= 1).mean() >= FAST_WITHIN1, name
     assert np.array_equal(fa[~unk], d["img"][~unk])
 
 
@@ -455,10 +455,10 @@ def test_device_path_refuses_a_caller_capture(fctx):
     assert np.array_equal(d_out.cpu().numpy().reshape(H, W), want)
 
 
-def test_big_window_kernel_forced_on_small_cases(ctx, fctx, monkeypatch):
+def test_big_window_kernel_forced_on_small_cases(ctx, fctx, tune_env):
     """The global-scratch big-window kernel, forced onto ordinary launches (TF_FORCE_BIG=1):
     byte-identical to the oracle in both modes (it computes with EXACT arithmetic)."""
-    monkeypatch.setenv("TF_FORCE_BIG", "1")
+    tune_env([ctx, fctx], TF_FORCE_BIG=1)
     rng = np.random.default_rng(77)
     for trial in range(16):
         w, h = int(rng.integers(6, 80)), int(rng.integers(6, 80))

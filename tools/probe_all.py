@@ -20,4 +20,4 @@ for c in cfgs:
         out, st = ctx.tiled(img, kn, wl.tiles, wl.overlap, wl.params)
         best = st if best is None or st.kernel_ms < best.kernel_ms else best
     print(f"c{c} {mode}: frames={wl.frames} kernel {best.kernel_ms:8.3f} ms blocks {best.blocks_processed:7d}"
-          f" -> {wl.pixels/best.kernel_ms/1e3:9.1f} Mpix/s kernel-only", flush=True)
+          f" -> {wl.pixels/best.kernel_ms/1e3:9.1f} Mpix/s kernel-only, refined {best.blocks_refined}", flush=True)
