@@ -61,8 +61,14 @@ typedef enum tf_status {
 typedef enum tf_mode {
   TF_MODE_EXACT = 0, /* IEEE binary64, reference operation order, no FMA:
                         output byte-identical to the reference CPU FSE   */
-  TF_MODE_FAST = 1   /* binary64 with FMA contraction in the spectral
-                        update: within the stated tolerance             */
+  TF_MODE_FAST = 1   /* binary64 throughout (DFTs, W, update, 64-bit
+                        argmax keys) with FMA contraction, on the Hermitian
+                        half spectrum; blocks whose greedy selection meets
+                        an argmax near-tie (2^-38 relative) or whose window
+                        is nearly empty are re-run in EXACT arithmetic.
+                        Within the north-star tolerance (>= 99.9 % of
+                        reconstructed pixels within +-1, |dPSNR| <= 0.05 dB;
+                        identical to EXACT on the c1-c5 frames measured) */
 } tf_mode;
 
 /* tiling.hpp:16-27 (Rect) */

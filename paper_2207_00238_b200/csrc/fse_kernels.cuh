@@ -235,8 +235,8 @@ struct WideLayout {
 
 // FAST pair kernel (full 16 x 16 windows, config 3): two blocks per warp, one per half-warp
 // (lane -> column k, all 9 half-spectrum rows per lane).  Per half:
-//   [region: W FP32 rows 0..S+HR-1 | staging (w FP32, w*v FP64) | C(x, l)] then, after both
-//   halves, [selection logs: 2 x (double2 + int32) x iters][twiddles][misc]
+//   [region: W rows 0..S+HR-1 (binary64 complex) | first C(x, l) of the DFT] then, after both
+//   halves, [selection logs: 2 x (double2 + int32) x iters][twiddles, rho^d][misc]
 struct PairLayout {
   int region, off_log, log_stride, off_tw, total;
   __host__ __device__ PairLayout(int S, int iters) {
