@@ -20,8 +20,18 @@ for mode in ("exact", "fast"):
         kn = np.stack(kns) if wl.frames > 1 else kns[0]
         for nb in ("1", "3"):
             os.environ["TF_STREAM_BANDS"] = nb
+            ctx.reload_tuning()
             out, st = ctx.tiled(img, kn, min(wl.tiles, 4), wl.overlap, wl.params)
             print(f"{mode} c{c} bands={nb}: blocks {st.blocks_processed}", flush=True)
+    # small symmetric windows with cell losses: argmax ties -> the FAST near-tie guard and
+    # its EXACT refinement launch run
+    rng = np.random.default_rng(5)
+    for trial in range(4):
+        cells = rng.random((20, 30)) > 0.3
+        kn = np.repeat(np.repeat(cells, 2, 0), 2, 1).astype(np.uint8)
+        img = rng.integers(0, 256, kn.shape, dtype=np.uint8)
+        out, st = ctx.tiled(img, kn, 2, 4, T.FseLiteParams(2, 2, 30, 0.5, 0.7))
+        print(f"{mode} tie case {trial}: blocks {st.blocks_processed} refined {st.blocks_refined}", flush=True)
     if mode == "fast":
         a, k = T.synth_frame(2, 0, 100, 80)
         q = ctx.quality(np.stack([a, a]), np.stack([out[0] if out.ndim == 3 else a, a]), None)
