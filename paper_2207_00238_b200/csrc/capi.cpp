@@ -460,7 +460,8 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   }
   // FAST half kernel: W rows + partial copy, log (20 B/iteration) reuses W's space after the loop
   const tfb::HalfLayout hlay(span, span, std::max(wbpt, 1), pl.wmax, hnt,
-                            tfb::half_slog(hnt, std::max(wbpt, 1), false) ? p.iters : 0);
+                            tfb::half_slog(hnt, std::max(wbpt, 1), false) ? p.iters : 0,
+                            tfb::half_nocopy(hnt, false));
   const bool hslog = tfb::half_slog(hnt, std::max(wbpt, 1), false);
   if (wkind == 2 && ((!hslog && 20 * p.iters > hlay.wbytes) || hlay.total > 227 * 1024)) wbpt = wkind = 0;
   const int wsmem = wkind == 2 ? hlay.total : wlay.total;

@@ -183,12 +183,21 @@ __host__ __device__ constexpr bool half_slog(int nt, int bpth, bool gen) {
   return !gen && nt == 32 && bpth <= 5;
 }
 
+#ifndef TF_HALF_NOCOPY
+#define TF_HALF_NOCOPY 1  // full-window one-warp kernels: W without the copy of rows 0..lmax (c2 1.054 -> 0.990 ms)
+#endif
+__host__ __device__ constexpr bool half_nocopy(int nt, bool gen) { return TF_HALF_NOCOPY && nt == 32 && !gen; }
+
 struct HalfLayout {
   int wbytes, off_tw, off_sync, off_log, total;
-  // log_iters > 0: room for the selection log (double2 + int32 per iteration) at off_log
-  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt, int log_iters = 0) {
+  // log_iters > 0: room for the selection log (double2 + int32 per iteration) at off_log.
+  // nocopy: W keeps rows 0..L-1 plus the few rows (lmax - L/2 + 1) that the second gather
+  // reaches past L-1; the first gather wraps by arithmetic instead of reading copy rows
+  __host__ __device__ HalfLayout(int M, int L, int bpth, int wmax, int nt, int log_iters = 0,
+                                 bool nocopy = false) {
     const int lmax = bpth * (nt / M) - 1;
-    const int rows = kHalfWB * M * (L + lmax + 1);
+    const int ncp = nocopy ? (lmax - L / 2 + 1 > 0 ? lmax - L / 2 + 1 : 0) : lmax + 1;
+    const int rows = kHalfWB * M * (L + ncp);
     int scratch = 48 * kHalfCY * wmax + 2 * M * L;  // DFT scratch overlaps W (written after)
     if (nt == 32 && M == L && scratch < 32 * bpth * 32)
       scratch = 32 * bpth * 32;  // TF_HALF_T2: C(x, l) of the half rows, values + weights (FP64)
