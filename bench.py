@@ -212,7 +212,7 @@ def ncu_profile(mode, config):
     if not files:
         return {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    traffic, smem, fp64, pipe, found = 0.0, [], 0.0, [], False
+    traffic, smem, fp64, pipe, fma32, found = 0.0, [], 0.0, [], [], False
     with open(files[-1]) as f:
         rows = list(csv.DictReader(f))
     for r in rows:
@@ -227,10 +227,12 @@ def ncu_profile(mode, config):
             fp64 += float(r["value"])
         if r["metric"] == "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active":
             pipe.append(round(float(r["value"]), 1))
+        if r["metric"] == "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active":
+            fma32.append(round(float(r["value"]), 1))
     if not found:
         return {}
     return {"traffic": int(traffic), "smem_pct": smem, "source": "profiles/" + Path(files[-1]).name,
-            "fp64_flops": fp64 or None, "fp64_pipe_pct": pipe}
+            "fp64_flops": fp64 or None, "fp64_pipe_pct": pipe, "fp32_pipe_pct": fma32}
 
 
 def main():
@@ -425,6 +427,8 @@ def main():
             "traffic_source": prof.get("source"),
             "smem_wavefront_pct_of_peak_ncu": prof.get("smem_pct"),
             "fp64_pipe_pct_of_peak_ncu": prof.get("fp64_pipe_pct"),
+            # FP32 FMA pipe per kernel (index arithmetic only: the FSE math is binary64)
+            "fp32_pipe_pct_of_peak_ncu": prof.get("fp32_pipe_pct"),
             "smem_peak_tbs": round(smem.value, 2),
             "kernel_share_of_step": round(mean_k / ms_step, 3)}
 
