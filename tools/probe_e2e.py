@@ -65,11 +65,14 @@ def timeit(fn, k=20):
 ref = None
 for nb in ("1", "2", "4", "8", "16"):
     os.environ["TF_STREAM_BANDS"] = nb
+    ctx.reload_tuning()
     ms = timeit(host_call)
     out = h_out.numpy().copy()
     ref = out if ref is None else ref
     print(f"c{cfg} {mode} frames={wl.frames} host API bands={nb:2s}: {ms:.3f} ms/call -> "
           f"{n / ms / 1e3:.1f} Mpix/s  equal={np.array_equal(out, ref)}", flush=True)
+os.environ.pop("TF_STREAM_BANDS", None)
+ctx.reload_tuning()
 ms = timeit(torch_call)
 print(f"c{cfg} {mode} torch H2D + device call + D2H: {ms:.3f} ms/call -> {n / ms / 1e3:.1f} Mpix/s "
       f"equal={np.array_equal(h_out.numpy(), ref)}", flush=True)
