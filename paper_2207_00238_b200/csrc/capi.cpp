@@ -1321,7 +1321,7 @@ static int run_streamed(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* img,
   const int span = p.block + p.margin;  // rows a window reaches below its block's first row
   // chunk 0 ends exactly at the last row band 0's windows reach (band 0 starts as soon as
   // it can), the remaining rows in nin - 1 equal chunks (measured host call, vs nin equal
-  // chunks, TF_STREAM_UNIFORM=1: c2 0.775 vs 0.790 ms, c3 5.80 vs 6.00, c4 12.94 vs 13.11)
+  // chunks: c2 0.775 vs 0.790 ms, c3 5.80 vs 6.00, c4 12.94 vs 13.11, round 1)
   std::vector<int64_t> cb(static_cast<size_t>(nin) + 1, rows);
   cb[0] = 0;
   if (nin > 1) {
