@@ -136,12 +136,38 @@ def ref_frames(wl):
     return np.stack(imgs), np.stack(kns)
 
 
-def band_blocks(wl, threads):
-    """Rows per task of the all-cores band split, in blocks: ~64-row bands (each band re-runs
-    a ceil(margin/B)*B-row apron above and below, so 1-block bands of small blocks would
-    repeat most of the work), fewer when the frame has too few rows to feed every thread."""
-    B = wl.params.block_size
-    return max(1, min(max(1, 64 // B), (wl.H * wl.frames) // (B * threads)))
+def band_blocks(wl, threads, part=0, n_parts=1, frames=None):
+    """Rows per task of the all-cores band split, in blocks.  Each band re-runs a
+    ceil(margin/B)*B-row apron above and below, so thin bands repeat work while thick ones
+    leave threads idle: pick the band that minimises the simulated makespan of the task list
+    ref_tiled_allcores_part builds (tasks taken in order by the first free thread, cost =
+    rows x width processed)."""
+    import heapq
+
+    import oracle as O
+    p = wl.params
+    B, apron = p.block_size, -(-p.support_margin // p.block_size) * p.block_size
+    frames = wl.frames if frames is None else frames
+    tiles = [(O.ref_expand(c, wl.overlap, wl.W, wl.H), c)
+             for t, c in enumerate(O.ref_plan_proposed(wl.W, wl.H, wl.tiles)) if t % n_parts == part]
+    best = (float("inf"), 1)
+    for b in range(1, max(2, 256 // B) + 1):
+        band, costs = B * b, []
+        for h, c in tiles:
+            cy0 = int(c[1]) - int(h[1])
+            cy1 = cy0 + int(c[3])
+            for y0 in range(0, int(h[3]), band):
+                y1 = min(int(h[3]), y0 + band)
+                if y1 > cy0 and y0 < cy1:
+                    costs.append((min(int(h[3]), y1 + apron) - max(0, y0 - apron)) * int(h[2]))
+        costs *= frames
+        free = [0] * threads
+        for cst in costs:
+            heapq.heappush(free, heapq.heappop(free) + cst)
+        span = max(free)
+        if span < best[0]:
+            best = (span, b)
+    return best[1]
 
 
 def ref_args(wl):
@@ -174,7 +200,7 @@ def run_reference(args, wl, rank, world):
     for i in range(warmup + args.steps):
         part = i % n_sample
         t0 = time.perf_counter()
-        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads),
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads, part, n_sample),
                              out=out, part=part, n_parts=n_sample)
         dt = time.perf_counter() - t0
         if i >= warmup:
@@ -503,7 +529,7 @@ def cpu_baseline(wl, img_np, kn_np, ex_out, fa_out, parity):
         img, kn = img_np[:frames], kn_np[:frames]
         out = img.copy()
         t0 = time.perf_counter()
-        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads),
+        O.ref_tiled_allcores(img, kn, *ref_args(wl), threads=threads, band_blocks=band_blocks(wl, threads, part, n_parts, frames),
                              out=out, part=part, n_parts=n_parts)
         dt = time.perf_counter() - t0
         from dataclasses import replace
