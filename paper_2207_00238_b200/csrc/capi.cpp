@@ -130,6 +130,7 @@ struct Gpu {
   int wocc_smem[2][33] = {};
   bool tw16_ok = false;       // c_tw16 uploaded on this device
   int pair_occ = 0, pair_smem = 0;  // FAST pair kernel (16x16 windows)
+  bool pair_acc = false;
   // CUDA graph of the device path: the second identical call (same buffers, shape, params,
   // stream, mode and tuning environment) is captured, later identical calls replay it
   cudaGraphExec_t gexec = nullptr;
@@ -493,14 +494,17 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   // FAST 16x16 full windows: the pair kernel (two blocks per warp; TF_NO_PAIR=1 keeps the
   // one-block-per-warp half kernel)
   int pair = 0, pair_smem = 0;
+  bool pair_acc = false;
   if (wkind == 2 && hnt == 32 && tfb::pair_supported(span) && !tu.no_pair) {
-    const tfb::PairLayout prl(span, p.iters);
+    pair_acc = p.block * p.block <= 16;  // a core pixel per lane: no selection log
+    const tfb::PairLayout prl(span, p.iters, pair_acc);
     if (prl.total <= 227 * 1024) {
-      if (g.pair_smem != prl.total) {
+      if (g.pair_smem != prl.total || g.pair_acc != pair_acc) {
         int occ = 0;
-        TF_CUDA(tfb::fse_pair_prepare(span, prl.total, &occ));
+        TF_CUDA(tfb::fse_pair_prepare(span, pair_acc, prl.total, &occ));
         g.pair_occ = occ;
         g.pair_smem = prl.total;
+        g.pair_acc = pair_acc;
       }
       if (g.pair_occ >= 1) {
         pair = span;
@@ -762,7 +766,7 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     if (pair) {
       const int pg = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(g.sms) * g.pair_occ,
                                                         std::max<int64_t>((cand + 1) / 2, 1)));
-      TF_CUDA(tfb::fse_pair_launch(pair, w, pg, pair_smem, s));
+      TF_CUDA(tfb::fse_pair_launch(pair, pair_acc, w, pg, pair_smem, s));
       ++g.kl;
     } else if (wkind == 1) {
       TF_CUDA(tfb::fse_warp_launch(wbpt, exact, w, wg, wsmem, s));

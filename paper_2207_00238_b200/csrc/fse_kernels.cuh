@@ -248,7 +248,9 @@ struct WideLayout {
 //   halves, [selection logs: 2 x (double2 + int32) x iters][twiddles, rho^d][misc]
 struct PairLayout {
   int region, off_log, log_stride, off_tw, total;
-  __host__ __device__ PairLayout(int S, int iters) {
+  // acc: the kernel's ACC variant accumulates the model at the core pixels in registers
+  // (blocks of at most 16 pixels) and keeps no selection log
+  __host__ __device__ PairLayout(int S, int iters, bool acc) {
     const int hr = S / 2 + 1;
     int r = 16 * S * (S + hr);                          // W rows 0..S-1 + copy of rows 0..hr-1 (FP64)
     const int stage = 16 * S * S, cx = 32 * hr * S;     // staging (w, w v); C(x, l) of both
@@ -256,7 +258,7 @@ struct PairLayout {
     r = r > cx ? r : cx;
     region = (r + 15) & ~15;
     off_log = 2 * region;
-    log_stride = (20 * iters + 15) & ~15;  // per half: double2 x iters, then int32 x iters
+    log_stride = acc ? 0 : (20 * iters + 15) & ~15;  // per half: double2 x iters, then int32 x iters
     off_tw = off_log + 2 * log_stride;
     total = off_tw + 32 * S + 16;
   }
@@ -309,8 +311,8 @@ cudaError_t quality_launch(const uint8_t* a, const uint8_t* b, const uint8_t* kn
                            double* ssim_sum, cudaStream_t s);
 // FAST pair kernel (S = 16 only; 0 if unsupported)
 int pair_supported(int S);
-cudaError_t fse_pair_prepare(int S, int smem_bytes, int* warps_per_sm);
-cudaError_t fse_pair_launch(int S, const FseLaunch& a, int grid, int smem_bytes, cudaStream_t s);
+cudaError_t fse_pair_prepare(int S, bool acc, int smem_bytes, int* warps_per_sm);
+cudaError_t fse_pair_launch(int S, bool acc, const FseLaunch& a, int grid, int smem_bytes, cudaStream_t s);
 cudaError_t enumerate_launch(const EnumLaunch& e, int max_grid_blocks, cudaStream_t s);
 cudaError_t cores_launch(uint8_t* frames, int W, int H, const TileDesc* tiles, int n_tiles,
                          int part, int n_parts, const int64_t* offs, uint8_t* packed, bool unpack,
