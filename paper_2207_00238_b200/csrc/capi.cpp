@@ -638,6 +638,9 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
   const bool guard = !exact && cfgx >= 0 && !tu.no_tie_guard;
   a.xlist = guard ? tblocks : nullptr;
   a.n_xlist = counters + 6;
+  // the pair kernel resolves its argmax on the keys' high words and relies on the near-tie
+  // list for the rest: without the guard the full windows stay on the half kernel
+  if (!guard) pair = 0;
   const auto launch_t = [&](cudaStream_t st) -> int {
     if (!guard) return TF_OK;
     tfb::FseLaunch x = a;
@@ -646,8 +649,11 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     x.next_block = counters + 7;
     x.stats = nullptr;  // their FAST pass is in the statistics
     x.xlist = nullptr;
-    // near-ties are rare (none on the c1-c5 frames): one CTA per SM, most exit at once
-    const int xg = static_cast<int>(std::min<int64_t>(g.sms, std::max<int64_t>(cand, 1)));
+    // near-ties are rare (c3: ~200 of 505,542 blocks in the pair kernel's 2^-20 band, none
+    // elsewhere on the c1-c5 frames): up to four CTAs per SM so that they run in one round;
+    // CTAs without a block exit at once
+    const int xg = static_cast<int>(std::min<int64_t>(
+        static_cast<int64_t>(g.sms) * std::min(g.occ[1][cfgx], 4), std::max<int64_t>(cand, 1)));
     TF_CUDA(tfb::fse_launch(cfgx, true, x, xg, xsmem, st));
     ++g.kl;
     return TF_OK;
