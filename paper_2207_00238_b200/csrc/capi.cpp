@@ -867,11 +867,13 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
       const bool x_list = q >= static_cast<size_t>(cnt[0] + cnt[2]);  // EXACT (hybrid): executed == F_b
       const bool warp_list = !x_list && q >= static_cast<size_t>(cnt[0]);
       if (pair && warp_list) {
-        // pair kernel: 9 half rows x 16 columns per block, DFT as the T2 scheme; every update
-        // runs both gathers (c2 = 0 when self-conjugate): 8 DFMA + |R|^2 (3) per bin
+        // pair kernel: 9 half rows x 16 columns per block; both DFT passes halved by their
+        // even / odd splits (4 M L HR + 8 Nh M); every update runs both gathers (c2 = 0 when
+        // self-conjugate): 8 DFMA + |R|^2 (3) per bin; the model term per iteration on all 16
+        // lanes of the half (ACC: DMUL + 2 DFMA) or the evaluation from the log
         const double Nh = static_cast<double>(b.L / 2 + 1) * b.M;
-        xfl += 8.0 * b.M * b.L * (b.L / 2 + 1) + 16.0 * Nh * b.M + 19.0 * Nh * b.iters +
-               11.0 * b.evaluated * b.iters;
+        xfl += 4.0 * b.M * b.L * (b.L / 2 + 1) + 8.0 * Nh * b.M + 19.0 * Nh * b.iters +
+               (pair_acc ? 5.0 * b.M * b.iters : 11.0 * b.evaluated * b.iters);
       } else if (wide && warp_list) {
         // wide kernel: pass 1 over y on the half rows (8 S^2 HR), pass 2 over x (16 Nh S),
         // loop and evaluation as the half kernel

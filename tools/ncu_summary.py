@@ -1,7 +1,7 @@
 """Summaries committed under profiles/: key metrics of one ncu --set full capture, and the
 per-kernel share of a `--metrics gpu__time_duration.sum` launch list.
 
-    python tools/ncu_summary.py full  gpurun_out/x.ncu-rep  profiles/rN_ncu_..._summary.csv
+    python tools/ncu_summary.py full  gpurun_out/x.ncu-rep  profiles/rN_ncu_..._summary.csv [first-n-launches]
     python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/rN_launches_....csv"""
 import csv
 import io
@@ -30,14 +30,14 @@ KEYS = [
 ]
 
 
-def full(rep, out):
+def full(rep, out, first=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "metric", "value", "unit"])
-        for r in rows[2:]:
+        for r in rows[2:2 + int(first)] if first else rows[2:]:
             d = dict(zip(hdr, r))
             u = dict(zip(hdr, units))
             for k in KEYS:
@@ -74,4 +74,4 @@ def launches(src, out):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"full": full, "launches": launches}[sys.argv[1]](*sys.argv[2:])
