@@ -182,10 +182,10 @@ namespace tfh {
 //                     known window pixels per unknown block pixel); TF_HYBRID=0 disables
 //   TF_NO_TIE_GUARD   FAST: no argmax near-tie refinement by the EXACT kernel
 //   TF_NO_PAIR, TF_NO_WIDE, TF_NO_GEN, TF_NO_WARP, TF_HALF_NT, TF_FORCE_BIG  kernel choice
-//   TF_VERBOSE, TF_KTIME, TF_PHASE_DUMP, TF_STREAM_DEBUG  diagnostics on stderr
+//   TF_VERBOSE, TF_KTIME, TF_STREAM_DEBUG  diagnostics on stderr
 struct Tune {
   bool no_graph = false, no_tie_guard = false, no_pair = false, no_wide = false, no_gen = false;
-  bool no_warp = false, force_big = false, verbose = false, ktime = false, phase_dump = false;
+  bool no_warp = false, force_big = false, verbose = false, ktime = false;
   bool stream_debug = false;
   int half_nt = 32, stream_bands = 0;        // 0: automatic
   float hybrid = 0.05f, hybrid_ratio = 1.5f;
@@ -201,7 +201,6 @@ struct Tune {
     force_big = on("TF_FORCE_BIG");
     verbose = on("TF_VERBOSE");
     ktime = on("TF_KTIME");
-    phase_dump = on("TF_PHASE_DUMP");
     stream_debug = on("TF_STREAM_DEBUG");
     half_nt = on("TF_HALF_NT") ? std::atoi(std::getenv("TF_HALF_NT")) : 32;
     stream_bands = on("TF_STREAM_BANDS") ? std::atoi(std::getenv("TF_STREAM_BANDS")) : 0;
@@ -899,23 +898,6 @@ static int run_device(tf_ctx* ctx, Gpu& g, const Plan& pl, const uint8_t* d_img,
     }
     res->flops = fl;
     res->flops_executed = xfl;
-    if (tu.phase_dump) {  // tuning aid (TF_PHASE_TIMING builds)
-      double c[4] = {0, 0, 0, 0};
-      for (const BlockStat& b : st)
-        for (int q = 0; q < 4; ++q) c[q] += b.cyc[q];
-      const double n = st.empty() ? 1.0 : static_cast<double>(st.size());
-      std::fprintf(stderr, "phase cycles/block: stage %.0f dft %.0f loop %.0f eval %.0f (%zu blocks)\n",
-                   c[0] / n, c[1] / n, c[2] / n, c[3] / n, st.size());
-      double ic[6] = {0, 0, 0, 0, 0, 0}, its = 0;
-      for (const BlockStat& b : st) {
-        for (int q = 0; q < 6; ++q) ic[q] += b.icyc[q];
-        its += b.iters;
-      }
-      its = its > 0 ? its : 1;
-      std::fprintf(stderr, "per-iteration cycles (thread 0): argmax %.0f reduce+coeff %.0f barrier %.0f "
-                   "decode %.0f bookkeeping %.0f update %.0f\n", ic[0] / its, ic[1] / its, ic[2] / its,
-                   ic[3] / its, ic[4] / its, ic[5] / its);
-    }
   }
   return TF_OK;
 }

@@ -30,9 +30,6 @@ struct BlockStat {
   int32_t pairs;     // non-self-conjugate selections P_b
   int32_t touched;   // touched bins T_b
   int32_t evaluated; // unknown core pixels evaluated (U_b restricted to the core)
-  int32_t cyc[4];    // TF_PHASE_TIMING builds: clock cycles of staging, DFT, loop, evaluate
-  int32_t icyc[6];   // TF_PHASE_TIMING builds, thread 0, summed over iterations: argmax,
-                     // warp-reduce+coeff+slot, barrier, slot-read+decode, bookkeeping, update
 };
 
 struct FseLaunch {
