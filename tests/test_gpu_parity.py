@@ -532,3 +532,46 @@ def test_degenerate_shapes_equal_oracle(ctx, fctx):
             assert st.blocks_reference == T.count_blocks(kn, B)
             fgot, _ = fctx.tiled(img, kn, 1, 0, _params(B, m, 20, 0.5, 0.8))
             assert np.abs(fgot.astype(int) - want.astype(int)).max() <= 1, f"fast {w}x{h} B={B} m={m}"
+
+
+@pytest.mark.parametrize("b,m", [(2, 7), (4, 6), (8, 4)])
+def test_pair_kernel_variants_against_exact_and_oracle(ctx, fctx, b, m):
+    """FAST on full 16x16 windows runs the pair kernel: its ACC variant (the model accumulated
+    at the core pixels, no selection log) for blocks of at most 16 pixels (B = 2, 4), the log
+    variant above (B = 8).  Each is held to the north-star tolerance against the oracle; the
+    statistics build (device call with stats) must write the same bytes as the plain one; the
+    near-tie band hands blocks to the EXACT kernel, so a mirror-symmetric mask -- exact
+    argmax ties in the reference -- still reproduces EXACT byte for byte."""
+    import torch
+    W, H, I = 200, 136, 30
+    img, kn = T.synth_frame(3, 11, W, H)  # i.i.d. pixel loss, p = 0.2
+    p = T.FseLiteParams(b, m, I, 0.5, 0.7)
+    want = O.tiled(img, kn, 2, m, b, m, I, 0.5, 0.7)[0]
+    ex, _ = ctx.tiled(img, kn, 2, m, p)
+    assert np.array_equal(ex, want)
+    fa, st = fctx.tiled(img, kn, 2, m, p)
+    unk = kn == 0
+    d = np.abs(fa.astype(int) - want.astype(int))[unk]
+    assert (d <= 1).mean() >= FAST_WITHIN1, f"B={b}: {(d > 1).sum()} of {d.size} pixels off by more than 1"
+    assert np.array_equal(fa[~unk], img[~unk])
+    # statistics build of the same kernels
+    d_img = torch.from_numpy(img.reshape(-1)).cuda()
+    d_kn = torch.from_numpy(kn.reshape(-1)).cuda()
+    d_out = torch.empty_like(d_img)
+    rs = fctx.tiled_device(d_img.data_ptr(), d_kn.data_ptr(), d_out.data_ptr(), W, H, 1, 2, m, p,
+                           want_stats=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().reshape(H, W), fa)
+    assert rs.blocks_processed == st.blocks_processed
+    # structured ties: a mask symmetric about both axes on a symmetric image
+    yy, xx = np.mgrid[0:64, 0:64]
+    simg = (128 + 60 * np.cos(2 * np.pi * (xx - 31.5) / 16) * np.cos(2 * np.pi * (yy - 31.5) / 8)).astype(np.uint8)
+    skn = np.ones((64, 64), np.uint8)
+    skn[24:40, 24:40] = 0
+    skn[28:36, 28:36] = 1
+    swant = O.fse_lite(simg, skn, b, m, I, 0.5, 0.7)
+    sex, _ = ctx.tiled(simg, skn, 1, 0, p)
+    assert np.array_equal(sex, swant)
+    sfa, sst = fctx.tiled(simg, skn, 1, 0, p)
+    sd = np.abs(sfa.astype(int) - swant.astype(int))[skn == 0]
+    assert (sd <= 1).mean() >= FAST_WITHIN1, f"symmetric case B={b}: {(sd > 1).sum()} of {sd.size} off, refined {sst.blocks_refined}"
