@@ -1533,11 +1533,11 @@ int tf_tiled_extrapolate(tf_ctx* ctx, const uint8_t* img, const uint8_t* known, 
   int nbands = 1;
   if (n == 1) {
     const int64_t rows = static_cast<int64_t>(frames) * H;
-    // measured per call (host API, pinned buffers; one-shot / best): c2 0.862 / 0.835 ms at
-    // 4 bands, c3 6.93 / 6.75 ms at 4-8, c4 15.24 / 14.17 ms at 8; the host enqueue costs
-    // ~25-35 us per band and banding adds ~5 % compute (smaller launches), so bands stay a
-    // few hundred rows tall
-    nbands = static_cast<int>(std::clamp<int64_t>(rows / 512, 1, 8));
+    // measured per call (host API, pinned buffers, round 2; bands 1 / 2 / 4 / 8): c2 1.15 /
+    // 1.07 / 1.05 / 1.07 ms, c3 5.89 / 5.72 / 5.77 / 5.87, c4 18.2 / 17.4 / 17.3 / 17.4; the host
+    // enqueue costs ~25-35 us per band and every band ends with its own border and refinement
+    // launches, so bands stay about a thousand rows tall
+    nbands = rows >= 1024 ? static_cast<int>(std::clamp<int64_t>(rows / 1024, 2, 8)) : 1;
     if (ctx->tune.stream_bands > 0) nbands = ctx->tune.stream_bands;
     nbands = std::max(1, std::min(nbands, Gpu::kMaxBands));
     if ((rows + nbands - 1) / nbands < p->block) nbands = 1;  // a block spans at most 2 bands
