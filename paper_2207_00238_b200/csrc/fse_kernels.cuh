@@ -217,7 +217,14 @@ struct HalfLayout {
 //   [twiddles: FP64 (cos, sin) x S, FP32 (cos, -sin) x S, FP32 (sin, cos) x S][slots][misc]
 struct WideLayout {
   int nt, g, hr, bp, rows, region, off_tw, off_slots, off_misc, total;
-  __host__ __device__ static constexpr int threads(int S) { return S <= 48 ? 192 : 256; }
+  // S <= 48: three warps per block (two row groups, 12-13 bins per thread).  The per-
+  // iteration argmax exchange costs every warp ~220 instructions whatever its share of the
+  // bins, so fewer, fatter warps win: 192 / 160 / 96 / 64 threads -> c4 16.3 / 16.4 / 14.2 /
+  // 15.7 ms, c5 (16 frames) 22.7 / 23.2 / 21.1 / 22.3 ms
+#ifndef TF_WIDE_NT48
+#define TF_WIDE_NT48 96
+#endif
+  __host__ __device__ static constexpr int threads(int S) { return S <= 48 ? TF_WIDE_NT48 : 256; }
   __host__ __device__ WideLayout(int S, int iters) {
     nt = threads(S);
     g = nt / S;
