@@ -244,6 +244,8 @@ def ncu_profile(mode, config):
     for r in rows:
         if "kernel" not in r or "fse" not in r["kernel"]:
             continue
+        if "nan" in r["value"]:  # a kernel whose counters ncu could not collect is left out
+            continue
         if r["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             traffic += float(r["value"]) * scale.get(r["unit"], 1)
             found = True

@@ -9,9 +9,10 @@ from paper_2207_00238_b200.configs import workload
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "exact"
 cfgs = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 3, 4, 5]
+c5_frames = int(sys.argv[3]) if len(sys.argv) > 3 else 16  # config 5 is a 64-frame batch
 ctx = T.Context(1, [0], mode)
 for c in cfgs:
-    wl = workload(c, frames=16 if c == 5 else None)
+    wl = workload(c, frames=c5_frames if c == 5 else None)
     imgs, kns = zip(*[T.synth_frame(c, f, wl.W, wl.H) for f in range(wl.frames)])
     img = np.stack(imgs) if wl.frames > 1 else imgs[0]
     kn = np.stack(kns) if wl.frames > 1 else kns[0]
